@@ -1,0 +1,159 @@
+"""Generate the golden fixtures under tests/golden/ from the LIVE reference.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py
+
+The fixtures pin the oracle (oracle/) to the reference; the GPU parity tests
+then compare the CUDA path with the oracle on the box, where the reference is
+absent. Outputs are small: hash tables, checksums, ADW bits, traces.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import skipm  # noqa: E402
+from skipm import ipm_core, krylov_solvers, preconditioning, sketching  # noqa: E402
+
+from paper_2209_08722_b200.problems import wide_dense_lp  # noqa: E402
+
+# (n, w, s, seed): s=1 CountSketch, Lemire rejections at large w, duplicate
+# redraws at s>1, and the 2s >= w argsort branch.
+HASH_CASES = [
+    (10_000, 400, 1, 11), (20_000, 4_000, 1, 12), (5_000, 3, 1, 13),
+    (3_000, 400, 18, 14), (2_000, 4_000, 20, 15), (500, 64, 8, 16),
+    (1_000, 40, 4, 17), (30, 8, 5, 18), (64, 12, 6, 19), (7, 7, 1, 20),
+    (1, 1, 1, 22),
+]
+BIG_HASH_CASES = [(1_000_000, 4_000, 1, 31), (1_000_000, 4_000, 4, 32),
+                  (4_000_000, 8_000, 1, 33)]
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def hashes():
+    out = {}
+    for (n, w, s, seed) in HASH_CASES:
+        W = sketching.build_sparse_embedding(n, w, s, seed)
+        key = f"{n}_{w}_{s}_{seed}"
+        out[f"cols_{key}"] = W.cols.astype(np.int64)
+        out[f"sign_{key}"] = (W.vals > 0).astype(np.int8)
+    # raw bounded draws with a high Lemire rejection rate (threshold 2^30)
+    for w in (3 * 2**30, 2**31 + 1, 5):
+        g = np.random.Generator(np.random.Philox(21))
+        out[f"lemire_{w}"] = g.integers(0, w, size=4000)
+    np.savez_compressed(os.path.join(HERE, "hashes.npz"), **out)
+    big = []
+    for (n, w, s, seed) in BIG_HASH_CASES:
+        W = sketching.build_sparse_embedding(n, w, s, seed)
+        big.append(dict(n=n, w=w, s=s, seed=seed,
+                        cols_sha256=sha(W.cols.astype(np.int64)),
+                        sign_sha256=sha((W.vals > 0).astype(np.int8)),
+                        cols_head=W.cols[:4].tolist(), cols_tail=W.cols[-4:].tolist()))
+    seeds = {}
+    for seed in (0, 1, 7, 12345):
+        g = np.random.Generator(np.random.Philox(seed))
+        key = np.random.SeedSequence(seed).generate_state(2, np.uint64)
+        seeds[str(seed)] = dict(key=[int(k) for k in key],
+                                draws=[int(g.integers(0, 2**63)) for _ in range(8)])
+    with open(os.path.join(HERE, "hashes_big.json"), "w") as f:
+        json.dump(dict(big=big, outer_seeds=seeds), f, indent=1)
+
+
+def adw():
+    out = {}
+    g = np.random.Generator(np.random.Philox(99))
+    m, n = 20, 600
+    A = g.standard_normal((m, n))
+    d = 10.0 ** g.uniform(-2, 1, n)
+    out["A"], out["d"] = A, d
+    lp = skipm.make_lp(A, np.zeros(m), np.ones(n))
+    for s in (1, 4):
+        W = sketching.build_sparse_embedding(n, 64, s, 100 + s)
+        out[f"adw_s{s}"] = sketching.apply_sketch(lp.A, d, W)
+        out[f"seed_s{s}"] = np.array(100 + s)
+    # normal operator and preconditioned CG on the same data
+    W = sketching.build_sparse_embedding(n, 64, 4, 104)
+    f = preconditioning.build_preconditioner(sketching.apply_sketch(lp.A, d, W),
+                                             sketch_tag=W.tag)
+    op = krylov_solvers.NormalOperator(lp.A, d)
+    v = g.standard_normal(m)
+    out["v"], out["normal_apply"] = v, op.apply(v)
+    dy, tr = krylov_solvers.pcg(op, f, v, 30, 1e-10)
+    out["pcg_dy"], out["pcg_norms"] = dy, np.array(tr.residual_norms)
+    out["inv_v"] = preconditioning.apply_inv(f, v)
+    out["pinv_v"] = preconditioning.apply_pinv_adw(f, v)
+    np.savez_compressed(os.path.join(HERE, "adw_small.npz"), **out)
+
+
+def c1_traces():
+    res = {}
+    lpd = wide_dense_lp(100, 10_000, 0)
+    lp = skipm.make_lp(lpd.A, lpd.b, lpd.c, name=lpd.name)
+    gamma = lpd.gamma_run(0.1)
+    for s_nnz in (4, 1):
+        start = ipm_core.make_iterate(lp, lpd.x0, lpd.y0, lpd.s0)
+        prm = ipm_core.IpmParams(mode="feasible", gamma=gamma, sigma=0.5, sketch="sparse",
+                                 w=400, s=s_nnz, tol_outer=1e-6, seed=0)
+        rep = ipm_core.solve(lp, start, prm)
+        d = rep.to_dict()
+        d.pop("params")
+        d["x_sha256"] = sha(rep.x)
+        d["x_head"] = rep.x[:8].tolist()
+        d["y"] = rep.y.tolist()
+        res[f"s{s_nnz}"] = d
+        print(f"c1 s={s_nnz}: outer {rep.outer} inner {rep.sum_inner} obj {rep.objective!r}")
+    res["gamma_run"] = gamma
+    with open(os.path.join(HERE, "c1_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
+def small_traces():
+    """A smaller LP (m=40, n=3000) in both modes, for fast lock-step checks."""
+    res = {}
+    lpd = wide_dense_lp(40, 3000, 5)
+    lp = skipm.make_lp(lpd.A, lpd.b, lpd.c, name=lpd.name)
+    for mode in ("feasible", "infeasible"):
+        start = ipm_core.make_iterate(lp, lpd.x0, lpd.y0, lpd.s0)
+        if mode == "feasible":
+            prm = ipm_core.IpmParams(mode=mode, gamma=lpd.gamma_run(0.1), sigma=0.5, w=160,
+                                     s=4, tol_outer=1e-7, seed=3)
+        else:
+            start = ipm_core.make_iterate(lp, np.ones(lp.n), np.zeros(lp.m), np.ones(lp.n))
+            prm = ipm_core.IpmParams(mode=mode, gamma=0.5, sigma=0.5, w=160, s=4,
+                                     tol_outer=1e-7, seed=4, max_outer=60)
+        try:
+            rep = ipm_core.solve(lp, start, prm)
+        except skipm.MaxIterations as e:
+            rep = e.report
+        d = rep.to_dict()
+        d.pop("params")
+        res[mode] = d
+        print(f"small {mode}: outer {rep.outer} conv {rep.converged} obj {rep.objective!r}")
+    with open(os.path.join(HERE, "small_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["hashes", "adw", "small", "c1"]
+    if "hashes" in what:
+        hashes()
+    if "adw" in what:
+        adw()
+    if "small" in what:
+        small_traces()
+    if "c1" in what:
+        c1_traces()
