@@ -1,0 +1,496 @@
+// K4/K8: single-pass column-streaming kernels over a dense column-major A.
+//
+// One template covers every A-pass of the hot path:
+//   normal    u = A (d2 .* (A' z))                 krylov_solvers.py:46-47
+//   gemv      u = A coef,  coef_j from n-vectors    ipm_core.py:99,204-206,502,223
+//   gemv_t    t = A' y (+ add - sub)                 ipm_core.py:100,218
+//   dir       A' dy -> ds, dx (elementwise) -> A dx  ipm_core.py:218-223 (one pass)
+//   iter      x+a dx, s+a ds, A' y_new + s_new - c, A x_new   ipm_core.py:94-102,308
+//
+// Layout: column j of A is A[j*lda .. j*lda+m) (lda even, 16-byte aligned), so a
+// group of cb consecutive columns is one contiguous range. Each warp owns a
+// private ring of `stages` shared-memory buffers filled by the TMA engine
+// (cp.async.bulk, L2 evict-first) and consumes one group per stage: lane l
+// holds rows 64k+2l, 64k+2l+1 in registers, the column dot is a warp
+// butterfly, and the rank-1 update accumulates into per-lane registers. A is
+// read from HBM exactly once per pass. Per-warp partial m-vectors are summed
+// in a fixed order per CTA, then across CTAs by skb_reduce_partials: the
+// result is deterministic run to run.
+#include <algorithm>
+
+#include "skb_common.cuh"
+#include "skb_internal.h"
+
+namespace skb {
+
+struct Pre {
+  double v[6];
+};
+
+SKB_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
+SKB_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+SKB_DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
+SKB_DEV double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ------------------------------------------------------------------- ops
+// Elementwise formulas use explicit round-to-nearest intrinsics in numpy's
+// evaluation order, so given equal inputs they are bit-identical to numpy.
+
+struct OpNormal {  // u += (d2_j * <a_j, z>) a_j
+  static constexpr bool kDot = true, kAxpy = true;
+  static constexpr int kPre = 1;
+  const double* d2;
+  SKB_DEV void load(int64_t j, Pre& p) const { p.v[0] = d2[j]; }
+  SKB_DEV double coef(int64_t, const Pre& p, double dot) const { return dmul(p.v[0], dot); }
+  SKB_DEV void emit(int64_t, const Pre&, double, double) const {}
+};
+
+struct OpGemvX {  // u += x_j a_j
+  static constexpr bool kDot = false, kAxpy = true;
+  static constexpr int kPre = 1;
+  const double* x;
+  SKB_DEV void load(int64_t j, Pre& p) const { p.v[0] = x[j]; }
+  SKB_DEV double coef(int64_t, const Pre& p, double) const { return p.v[0]; }
+  SKB_DEV void emit(int64_t, const Pre&, double, double) const {}
+};
+
+struct OpGemvRatio {  // u += (v_j / s_j) a_j          (ipm_core.py:502)
+  static constexpr bool kDot = false, kAxpy = true;
+  static constexpr int kPre = 2;
+  const double* v;
+  const double* s;
+  SKB_DEV void load(int64_t j, Pre& p) const {
+    p.v[0] = v[j];
+    p.v[1] = s[j];
+  }
+  SKB_DEV double coef(int64_t, const Pre& p, double) const { return ddiv(p.v[0], p.v[1]); }
+  SKB_DEV void emit(int64_t, const Pre&, double, double) const {}
+};
+
+struct OpRhs {  // u_j = x - smu/s [- (x/s) r_d]       (ipm_core.py:202-206)
+  static constexpr bool kDot = false, kAxpy = true;
+  static constexpr int kPre = 3;
+  const double *x, *s, *rd;  // rd == nullptr: feasible mode
+  double smu;
+  SKB_DEV void load(int64_t j, Pre& p) const {
+    p.v[0] = x[j];
+    p.v[1] = s[j];
+    p.v[2] = rd ? rd[j] : 0.0;
+  }
+  SKB_DEV double coef(int64_t, const Pre& p, double) const {
+    double u = dsub(p.v[0], ddiv(smu, p.v[1]));
+    if (rd) u = dsub(u, dmul(ddiv(p.v[0], p.v[1]), p.v[2]));
+    return u;
+  }
+  SKB_DEV void emit(int64_t, const Pre&, double, double) const {}
+};
+
+struct OpGemvT {  // out_j = (<a_j, y> + add_j) - sub_j
+  static constexpr bool kDot = true, kAxpy = false;
+  static constexpr int kPre = 2;
+  const double *add, *sub;
+  double* out;
+  SKB_DEV void load(int64_t j, Pre& p) const {
+    p.v[0] = add ? add[j] : 0.0;
+    p.v[1] = sub ? sub[j] : 0.0;
+  }
+  SKB_DEV double coef(int64_t, const Pre&, double) const { return 0.0; }
+  SKB_DEV void emit(int64_t j, const Pre& p, double dot, double) const {
+    double t = dot;
+    if (add) t = dadd(t, p.v[0]);
+    if (sub) t = dsub(t, p.v[1]);
+    out[j] = t;
+  }
+};
+
+struct OpDir {  // assemble_directions in one pass (ipm_core.py:218-223)
+  static constexpr bool kDot = true, kAxpy = true;
+  static constexpr int kPre = 4;
+  const double *x, *s, *v, *rd;  // rd == nullptr: feasible mode
+  double smu;
+  double *ds_out, *dx_out, *atdy_out;
+  SKB_DEV void load(int64_t j, Pre& p) const {
+    p.v[0] = x[j];
+    p.v[1] = s[j];
+    p.v[2] = v[j];
+    p.v[3] = rd ? rd[j] : 0.0;
+  }
+  SKB_DEV double ds_of(const Pre& p, double atdy) const {
+    return rd ? dsub(-p.v[3], atdy) : -atdy;
+  }
+  SKB_DEV double coef(int64_t, const Pre& p, double dot) const {
+    const double ds = ds_of(p, dot);
+    const double xs = ddiv(p.v[0], p.v[1]);
+    double dx = dadd(-p.v[0], ddiv(smu, p.v[1]));
+    dx = dsub(dx, dmul(xs, ds));
+    return dsub(dx, ddiv(p.v[2], p.v[1]));
+  }
+  SKB_DEV void emit(int64_t j, const Pre& p, double dot, double dx) const {
+    ds_out[j] = ds_of(p, dot);
+    dx_out[j] = dx;
+    if (atdy_out) atdy_out[j] = dot;
+  }
+};
+
+struct OpIter {  // make_iterate at x + a dx, y_new (=z), s + a ds (ipm_core.py:94-102)
+  static constexpr bool kDot = true, kAxpy = true;
+  static constexpr int kPre = 5;
+  const double *x, *dx, *s, *ds, *c;
+  double alpha;
+  double *x_out, *s_out, *rd_out;
+  SKB_DEV void load(int64_t j, Pre& p) const {
+    p.v[0] = x[j];
+    p.v[1] = dx ? dx[j] : 0.0;
+    p.v[2] = s[j];
+    p.v[3] = ds ? ds[j] : 0.0;
+    p.v[4] = c[j];
+  }
+  SKB_DEV double xnew(const Pre& p) const { return dx ? dadd(p.v[0], dmul(alpha, p.v[1])) : p.v[0]; }
+  SKB_DEV double snew(const Pre& p) const { return ds ? dadd(p.v[2], dmul(alpha, p.v[3])) : p.v[2]; }
+  SKB_DEV double coef(int64_t, const Pre& p, double) const { return xnew(p); }
+  SKB_DEV void emit(int64_t j, const Pre& p, double dot, double xn) const {
+    const double sn = snew(p);
+    if (x_out) x_out[j] = xn;
+    if (s_out) s_out[j] = sn;
+    rd_out[j] = dsub(dadd(dot, sn), p.v[4]);
+  }
+};
+
+// --------------------------------------------------------------- kernel
+
+template <int R2, bool ZREG, class Op>
+__global__ void __launch_bounds__(256, 1)
+    colstream_kernel(const double* __restrict__ A, int64_t lda, int m, int64_t n, int cb,
+                     int stages, int64_t ngroups, const double* __restrict__ z,
+                     double* __restrict__ part, Op op) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t col_bytes = (size_t)lda * 8, stage_bytes = (size_t)cb * col_bytes;
+  double* zs = reinterpret_cast<double*>(smem);
+  size_t off = (((size_t)m * 8) + 127) & ~(size_t)127;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off);
+  off += (((size_t)nw * 4 * 8) + 127) & ~(size_t)127;
+  unsigned char* bufs = smem + off;
+
+  if (Op::kDot && !ZREG)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) zs[i] = z[i];
+  uint64_t* mybar = bars + warp * 4;
+  unsigned char* mybuf = bufs + (size_t)warp * stages * stage_bytes;
+  if (lane == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&mybar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  double zr[ZREG ? 2 * R2 : 1];
+  double acc[Op::kAxpy ? 2 * R2 : 1];
+#pragma unroll
+  for (int k = 0; k < R2; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int r = 64 * k + 2 * lane + e;
+      if (ZREG && Op::kDot) zr[2 * k + e] = r < m ? z[r] : 0.0;
+      if (Op::kAxpy) acc[2 * k + e] = 0.0;
+    }
+  }
+
+  const int64_t gw = (int64_t)blockIdx.x * nw + warp, GW = (int64_t)gridDim.x * nw;
+  const int64_t my = gw < ngroups ? (ngroups - 1 - gw) / GW + 1 : 0;
+  const uint64_t pol = l2_evict_first_policy();
+
+  auto issue = [&](int64_t i, int st) {
+    const int64_t c0 = (gw + i * GW) * cb;
+    const int cnt = (int)min((int64_t)cb, n - c0);
+    const uint32_t bytes = (uint32_t)(cnt * col_bytes);
+    mbar_arrive_expect_tx(&mybar[st], bytes);
+    bulk_g2s(mybuf + st * stage_bytes, A + c0 * lda, bytes, &mybar[st], pol);
+  };
+  if (lane == 0)
+    for (int64_t i = 0; i < min((int64_t)stages, my); ++i) issue(i, (int)i);
+
+  for (int64_t i = 0; i < my; ++i) {
+    const int st = (int)(i % stages);
+    const uint32_t ph = (uint32_t)((i / stages) & 1);
+    const int64_t c0 = (gw + i * GW) * cb;
+    const int cnt = (int)min((int64_t)cb, n - c0);
+    Pre pre;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) pre.v[q] = 0.0;
+    if (lane < cnt) op.load(c0 + lane, pre);
+    mbar_wait(&mybar[st], ph);
+    const double* buf = reinterpret_cast<const double*>(mybuf + st * stage_bytes);
+    for (int c = 0; c < cnt; ++c) {
+      const double* col = buf + (size_t)c * lda;
+      if constexpr (!ZREG) {
+        // large m: stream the column from shared memory twice (dot, then axpy)
+        double dot = 0.0;
+        if (Op::kDot) {
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll 8
+          for (int k = 0; k < R2; ++k) {
+            const int r = 64 * k + 2 * lane;
+            if (r < m) {
+              const double2 t = *reinterpret_cast<const double2*>(col + r);
+              d0 = fma(t.x, zs[r], d0);
+              if (r + 1 < m) d1 = fma(t.y, zs[r + 1], d1);
+            }
+          }
+          dot = warp_sum(d0 + d1);
+        }
+        Pre pc;
+#pragma unroll
+        for (int q = 0; q < Op::kPre; ++q) pc.v[q] = __shfl_sync(0xffffffffu, pre.v[q], c);
+        const double cf = op.coef(c0 + c, pc, dot);
+        if (lane == 0) op.emit(c0 + c, pc, dot, cf);
+        if (Op::kAxpy) {
+#pragma unroll
+          for (int k = 0; k < R2; ++k) {
+            const int r = 64 * k + 2 * lane;
+            double2 t = make_double2(0.0, 0.0);
+            if (r < m) {
+              t = *reinterpret_cast<const double2*>(col + r);
+              if (r + 1 >= m) t.y = 0.0;
+            }
+            acc[2 * k] = fma(cf, t.x, acc[2 * k]);
+            acc[2 * k + 1] = fma(cf, t.y, acc[2 * k + 1]);
+          }
+        }
+        continue;
+      }
+      double2 a[R2];
+#pragma unroll
+      for (int k = 0; k < R2; ++k) {
+        const int r = 64 * k + 2 * lane;
+        double2 t = make_double2(0.0, 0.0);
+        if (r < m) {
+          t = *reinterpret_cast<const double2*>(col + r);
+          if (r + 1 >= m) t.y = 0.0;
+        }
+        a[k] = t;
+      }
+      double dot = 0.0;
+      if (Op::kDot) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R2; ++k) {
+          const int r = 64 * k + 2 * lane;
+          const double z0 = ZREG ? zr[2 * k] : (r < m ? zs[r] : 0.0);
+          const double z1 = ZREG ? zr[2 * k + 1] : (r + 1 < m ? zs[r + 1] : 0.0);
+          d0 = fma(a[k].x, z0, d0);
+          d1 = fma(a[k].y, z1, d1);
+        }
+        dot = warp_sum(d0 + d1);
+      }
+      Pre pc;
+#pragma unroll
+      for (int q = 0; q < Op::kPre; ++q) pc.v[q] = __shfl_sync(0xffffffffu, pre.v[q], c);
+      const double cf = op.coef(c0 + c, pc, dot);
+      if (lane == 0) op.emit(c0 + c, pc, dot, cf);
+      if (Op::kAxpy) {
+#pragma unroll
+        for (int k = 0; k < R2; ++k) {
+          acc[2 * k] = fma(cf, a[k].x, acc[2 * k]);
+          acc[2 * k + 1] = fma(cf, a[k].y, acc[2 * k + 1]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && i + stages < my) issue(i + stages, st);
+  }
+
+  if (!Op::kAxpy) return;
+  __syncthreads();  // every warp is done with its stage buffers
+  double* red = reinterpret_cast<double*>(bufs);
+#pragma unroll
+  for (int k = 0; k < R2; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int r = 64 * k + 2 * lane + e;
+      if (r < m) red[(size_t)warp * m + r] = acc[2 * k + e];
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[(size_t)w * m + r];
+    part[(size_t)blockIdx.x * m + r] = s;
+  }
+}
+
+// out[i] = sum_b part[b][i] (fixed order: 8 interleaved slices, combined in order) - sub[i]
+__global__ void reduce_partials_kernel(const double* __restrict__ part, int nb, int m,
+                                       const double* __restrict__ sub, double* __restrict__ out) {
+  __shared__ double sm[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int r = blockIdx.x * 32 + tx;
+  double s = 0.0;
+  if (r < m)
+    for (int b = ty; b < nb; b += 8) s += part[(size_t)b * m + r];
+  sm[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && r < m) {
+    double t = ((sm[0][tx] + sm[1][tx]) + (sm[2][tx] + sm[3][tx])) +
+               ((sm[4][tx] + sm[5][tx]) + (sm[6][tx] + sm[7][tx]));
+    out[r] = sub ? __dsub_rn(t, sub[r]) : t;
+  }
+}
+
+// ------------------------------------------------------------- launching
+
+struct StreamCfg {
+  int nw, stages, cb, grid;
+  size_t smem;
+  int64_t ngroups;
+};
+
+static StreamCfg stream_cfg(int m, int64_t n, int64_t lda) {
+  StreamCfg c;
+  const size_t col_bytes = (size_t)lda * 8;
+  c.cb = (int)std::max<size_t>(1, std::min<size_t>(32, 8192 / col_bytes));
+  const size_t stage_bytes = (size_t)c.cb * col_bytes;
+  const size_t zb = (((size_t)m * 8) + 127) & ~(size_t)127;
+  const size_t budget = 220 * 1024 - zb - 256;
+  c.nw = 8;
+  while (c.nw > 1 && (size_t)c.nw * 2 * stage_bytes > budget) c.nw >>= 1;
+  c.stages = (int)std::min<size_t>(4, budget / ((size_t)c.nw * stage_bytes));
+  size_t bufb = (size_t)c.nw * c.stages * stage_bytes;
+  bufb = std::max(bufb, (size_t)c.nw * m * 8);  // epilogue reuse
+  c.smem = zb + 256 + bufb;
+  c.ngroups = (n + c.cb - 1) / c.cb;
+  const int64_t need = (c.ngroups + c.nw - 1) / c.nw;
+  c.grid = (int)std::max<int64_t>(1, std::min<int64_t>(skb_num_sms(), need));
+  return c;
+}
+
+template <int R2, bool ZREG, class Op>
+static int launch_r2(const StreamCfg& c, const double* A, int64_t lda, int m, int64_t n,
+                     const double* z, double* part, const Op& op, cudaStream_t st) {
+  auto kern = colstream_kernel<R2, ZREG, Op>;
+  static size_t configured = 0;
+  if (c.smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) !=
+        cudaSuccess)
+      return SKB_ERR_CUDA;
+    configured = c.smem;
+  }
+  kern<<<c.grid, c.nw * 32, c.smem, st>>>(A, lda, m, n, c.cb, c.stages, c.ngroups, z, part, op);
+  return 0;
+}
+
+template <class Op>
+static int run_stream(const double* A, int64_t lda, int m, int64_t n, const double* z,
+                      double* out, const double* sub, const Op& op, skb_ws* ws,
+                      cudaStream_t st) {
+  if (m < 1 || n < 0 || lda < m || (lda & 1) || ((uintptr_t)A & 15)) return SKB_ERR_ARG;
+  if (m > 2048) return SKB_ERR_UNSUPPORTED;
+  if (n == 0) {
+    if (Op::kAxpy) {
+      if (sub) {
+        reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(nullptr, 0, m, sub, out);
+      } else {
+        cudaMemsetAsync(out, 0, (size_t)m * 8, st);
+      }
+    }
+    return 0;
+  }
+  const StreamCfg c = stream_cfg(m, n, lda);
+  double* part = nullptr;
+  if (Op::kAxpy) {
+    part = (double*)skb_ws_take(ws, (size_t)c.grid * m * 8);
+    if (!part) return SKB_ERR_WORKSPACE;
+  }
+  int rc;
+  if (m <= 64)
+    rc = launch_r2<1, true>(c, A, lda, m, n, z, part, op, st);
+  else if (m <= 128)
+    rc = launch_r2<2, true>(c, A, lda, m, n, z, part, op, st);
+  else if (m <= 256)
+    rc = launch_r2<4, true>(c, A, lda, m, n, z, part, op, st);
+  else if (m <= 512)
+    rc = launch_r2<8, true>(c, A, lda, m, n, z, part, op, st);
+  else if (m <= 1024)
+    rc = launch_r2<16, true>(c, A, lda, m, n, z, part, op, st);
+  else
+    rc = launch_r2<32, false>(c, A, lda, m, n, z, part, op, st);
+  if (rc) return rc;
+  if (Op::kAxpy)
+    reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, c.grid, m, sub, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : SKB_ERR_CUDA;
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+#define SKB_WS skb_ws ws = skb_ws_make(workspace, ws_bytes)
+
+extern "C" int skb_normal_apply(const double* A, int64_t m, int64_t n, int64_t lda,
+                                const double* d2, const double* z, double* u, const double* sub,
+                                void* workspace, size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpNormal op{d2};
+  return run_stream(A, lda, (int)m, n, z, u, sub, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_gemv(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,
+                        double* u, const double* sub, void* workspace, size_t ws_bytes,
+                        void* stream) {
+  SKB_WS;
+  OpGemvX op{x};
+  return run_stream(A, lda, (int)m, n, nullptr, u, sub, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_gemv_ratio(const double* A, int64_t m, int64_t n, int64_t lda,
+                              const double* v, const double* s, double* u, const double* sub,
+                              void* workspace, size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpGemvRatio op{v, s};
+  return run_stream(A, lda, (int)m, n, nullptr, u, sub, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_rhs(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,
+                       const double* s, const double* r_d, double sigma_mu, double* p,
+                       const double* r_p, void* workspace, size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpRhs op{x, s, r_d, sigma_mu};
+  return run_stream(A, lda, (int)m, n, nullptr, p, r_p, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_gemv_t(const double* A, int64_t m, int64_t n, int64_t lda, const double* y,
+                          const double* add, const double* sub, double* t, void* workspace,
+                          size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpGemvT op{add, sub, t};
+  return run_stream(A, lda, (int)m, n, y, nullptr, nullptr, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_directions(const double* A, int64_t m, int64_t n, int64_t lda,
+                              const double* dy, const double* x, const double* s,
+                              const double* v, const double* r_d, double sigma_mu, double* ds,
+                              double* dx, double* atdy, double* adx, void* workspace,
+                              size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpDir op{x, s, v, r_d, sigma_mu, ds, dx, atdy};
+  return run_stream(A, lda, (int)m, n, dy, adx, nullptr, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_iterate(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,
+                           const double* dx, const double* s, const double* ds, double alpha,
+                           const double* y_new, const double* b, const double* c,
+                           double* x_out, double* s_out, double* r_p, double* r_d,
+                           void* workspace, size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpIter op{x, dx, s, ds, c, alpha, x_out, s_out, r_d};
+  return run_stream(A, lda, (int)m, n, y_new, r_p, b, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_reduce_partials(const double* part, int32_t nparts, int64_t m,
+                                   const double* sub, double* out, void* stream) {
+  reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, (cudaStream_t)stream>>>(
+      part, nparts, (int)m, sub, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : SKB_ERR_CUDA;
+}
+
+extern "C" size_t skb_stream_workspace_bytes(int64_t m) {
+  return (size_t)skb_num_sms() * (size_t)m * 8 + 256;
+}

@@ -1,0 +1,151 @@
+"""Thin typed wrappers over the libskb C ABI (device tensors in, device tensors out).
+
+Each wrapper names the reference call it replaces. Higher layers
+(sketching, krylov_solvers, ipm_core) only talk to the device through here.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .runtime import F64, lda_for, require_cuda, stream_ptr, workspace
+
+
+class DeviceMatrix:
+    """Dense A (m x n) stored column-major on the device.
+
+    `cols` is a (n, lda) float64 tensor whose row j is column j of A (zero
+    padded to lda = m rounded up to even). Column blocks are contiguous so the
+    streaming kernels move them with the TMA bulk engine."""
+
+    def __init__(self, cols: torch.Tensor, m: int):
+        assert cols.dtype == F64 and cols.is_cuda and cols.dim() == 2
+        assert cols.shape[1] == lda_for(m) and cols.is_contiguous()
+        self.cols = cols
+        self.m = int(m)
+        self.n = int(cols.shape[0])
+        self.lda = int(cols.shape[1])
+
+    @property
+    def shape(self):
+        return (self.m, self.n)
+
+    @classmethod
+    def from_host(cls, A, device=None) -> "DeviceMatrix":
+        """A: numpy (m x n) dense, or a scipy sparse matrix (densified)."""
+        device = device or require_cuda()
+        if hasattr(A, "toarray"):
+            A = A.toarray()
+        A = np.asarray(A, dtype=np.float64)
+        m, n = A.shape
+        cols = torch.zeros((n, lda_for(m)), dtype=F64, device=device)
+        step = max(1, (1 << 28) // max(1, 8 * m))  # upload in ~256 MB column slabs
+        for j0 in range(0, n, step):
+            j1 = min(n, j0 + step)
+            blk = torch.from_numpy(np.ascontiguousarray(A[:, j0:j1].T))
+            cols[j0:j1, :m].copy_(blk, non_blocking=False)
+        return cls(cols, m)
+
+    @classmethod
+    def from_rows_device(cls, A_rows: torch.Tensor) -> "DeviceMatrix":
+        """A given as a (m x n) row-major device tensor."""
+        m, n = A_rows.shape
+        cols = torch.zeros((n, lda_for(m)), dtype=F64, device=A_rows.device)
+        cols[:, :m].copy_(A_rows.t())
+        return cls(cols, m)
+
+    def column_slice(self, j0: int, j1: int) -> "DeviceMatrix":
+        return DeviceMatrix(self.cols[j0:j1], self.m)
+
+    def to_host(self) -> np.ndarray:
+        return self.cols[:, : self.m].t().contiguous().cpu().numpy()
+
+
+def _ws(m: int, extra: int = 0):
+    need = int(_lib.lib().skb_stream_workspace_bytes(m)) + extra
+    return workspace(need)
+
+
+def _p(t):
+    return None if t is None else t
+
+
+def normal_apply(A: DeviceMatrix, d2, z, out, sub=None):
+    """out = A (d2 .* (A' z)) [- sub]   (krylov_solvers.py:46-47)."""
+    ws, cap = _ws(A.m)
+    _lib.call("skb_normal_apply", A.cols, A.m, A.n, A.lda, d2, z, out, _p(sub), ws, cap,
+              stream_ptr())
+    return out
+
+
+def gemv(A: DeviceMatrix, x, out, sub=None):
+    """out = A x [- sub]   (lp.A @ x, ipm_core.py:99)."""
+    ws, cap = _ws(A.m)
+    _lib.call("skb_gemv", A.cols, A.m, A.n, A.lda, x, out, _p(sub), ws, cap, stream_ptr())
+    return out
+
+
+def gemv_ratio(A: DeviceMatrix, v, s, out, sub=None):
+    """out = A (v / s) [- sub]   (ipm_core.py:502)."""
+    ws, cap = _ws(A.m)
+    _lib.call("skb_gemv_ratio", A.cols, A.m, A.n, A.lda, v, s, out, _p(sub), ws, cap,
+              stream_ptr())
+    return out
+
+
+def rhs(A: DeviceMatrix, x, s, sigma_mu: float, out, r_d=None, r_p=None):
+    """build_rhs (ipm_core.py:196-206)."""
+    ws, cap = _ws(A.m)
+    _lib.call("skb_rhs", A.cols, A.m, A.n, A.lda, x, s, _p(r_d), float(sigma_mu), out, _p(r_p),
+              ws, cap, stream_ptr())
+    return out
+
+
+def gemv_t(A: DeviceMatrix, y, out, add=None, sub=None):
+    """out = (A' y [+ add]) [- sub]   (ipm_core.py:100,218)."""
+    ws, cap = _ws(A.m)
+    _lib.call("skb_gemv_t", A.cols, A.m, A.n, A.lda, y, _p(add), _p(sub), out, ws, cap,
+              stream_ptr())
+    return out
+
+
+def directions(A: DeviceMatrix, dy, x, s, v, sigma_mu, ds, dx, adx, atdy=None, r_d=None):
+    """assemble_directions' A-passes in one sweep (ipm_core.py:218-223)."""
+    ws, cap = _ws(A.m)
+    _lib.call("skb_directions", A.cols, A.m, A.n, A.lda, dy, x, s, v, _p(r_d), float(sigma_mu),
+              ds, dx, _p(atdy), adx, ws, cap, stream_ptr())
+
+
+def iterate(A: DeviceMatrix, x, s, y_new, b, c, r_p, r_d, dx=None, ds=None, alpha=0.0,
+            x_out=None, s_out=None):
+    """make_iterate's A-passes in one sweep (ipm_core.py:94-102)."""
+    ws, cap = _ws(A.m)
+    _lib.call("skb_iterate", A.cols, A.m, A.n, A.lda, x, _p(dx), s, _p(ds), float(alpha), y_new,
+              b, c, _p(x_out), _p(s_out), r_p, r_d, ws, cap, stream_ptr())
+
+
+def sparse_embedding(key0: int, key1: int, n: int, w: int, s: int, device=None):
+    """build_sparse_embedding's draws (sketching.py:104-117) -> (cols int32 (n,s), vals f64 (n,s), words)."""
+    device = device or require_cuda()
+    cols = torch.empty((n, s), dtype=torch.int32, device=device)
+    vals = torch.empty((n, s), dtype=F64, device=device)
+    ws_need = 64 * n * max(s, 1) + (1 << 20)
+    ws, cap = workspace(ws_need)
+    used = np.zeros(1, dtype=np.uint64)
+    _lib.call("skb_sparse_embedding", key0, key1, n, w, s, cols, vals, used.ctypes.data, ws, cap,
+              stream_ptr())
+    return cols, vals, int(used[0])
+
+
+def lemire_draw(key0: int, key1: int, bound: int, count: int, word_offset: int = 0,
+                device=None):
+    """rng.integers(0, bound, count) from 32-bit word `word_offset` -> (uint32 as int64, words)."""
+    device = device or require_cuda()
+    out = torch.empty(count, dtype=torch.int32, device=device)
+    ws, cap = workspace(64 * count + (1 << 20))
+    used = np.zeros(1, dtype=np.uint64)
+    _lib.call("skb_lemire_draw", key0, key1, word_offset, bound, count, out, used.ctypes.data, ws,
+              cap, stream_ptr())
+    return out.to(torch.int64) & 0xFFFFFFFF, int(used[0])

@@ -1,0 +1,74 @@
+"""Device plumbing: CUDA device/stream, workspace, pinned scalar readback.
+
+PyTorch is used only as the allocator and stream provider; every arithmetic
+operation on the hot path is a libskb kernel.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+
+F64 = torch.float64
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2209_08722_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    _lib.lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Workspace:
+    """Grow-only device scratch buffer shared by consecutive (stream-ordered) calls."""
+
+    def __init__(self):
+        self._buf = None
+        self._lock = threading.Lock()
+
+    def get(self, nbytes: int):
+        with self._lock:
+            if self._buf is None or self._buf.numel() < nbytes:
+                n = max(int(nbytes), 1 << 20)
+                n = 1 << (n - 1).bit_length()
+                self._buf = torch.empty(n, dtype=torch.uint8, device=require_cuda())
+            return self._buf, self._buf.numel()
+
+
+_WS = threading.local()
+
+
+def workspace(nbytes: int):
+    """-> (tensor, capacity) for the calling thread's workspace."""
+    w = getattr(_WS, "ws", None)
+    if w is None:
+        w = _WS.ws = Workspace()
+    return w.get(nbytes)
+
+
+class Scalars:
+    """A small device buffer of doubles read back through pinned memory."""
+
+    def __init__(self, n: int):
+        dev = require_cuda()
+        self.dev = torch.zeros(n, dtype=F64, device=dev)
+        self.host = torch.zeros(n, dtype=F64, pin_memory=True)
+
+    def fetch(self) -> np.ndarray:
+        self.host.copy_(self.dev, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.host.numpy().copy()
+
+
+def lda_for(m: int) -> int:
+    """Column stride of the device layout: even, so every column is 16-byte aligned."""
+    return m + (m & 1)

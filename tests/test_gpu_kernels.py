@@ -1,0 +1,184 @@
+"""GPU parity of the individual kernels against the oracle / golden fixtures."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import GOLDEN
+from oracle import chash
+from oracle import ipm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def K():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2209_08722_b200 import kernels
+    return kernels
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def _h(t):
+    return t.detach().cpu().numpy()
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ----------------------------------------------------------------- hashes
+
+
+def test_hash_tables_bit_exact(K):
+    g = np.load(os.path.join(GOLDEN, "hashes.npz"))
+    for key in g.files:
+        if not key.startswith("cols_"):
+            continue
+        n, w, s, seed = map(int, key[5:].split("_"))
+        k0, k1 = chash.philox_key(seed)
+        cols, vals, used = K.sparse_embedding(k0, k1, n, w, s)
+        assert np.array_equal(_h(cols).astype(np.int64), g[key]), (n, w, s, seed)
+        assert np.array_equal(_h(vals) > 0, g["sign_" + key[5:]].astype(bool))
+        assert np.all(np.abs(_h(vals)) == 1.0 / np.sqrt(s))
+
+
+def test_hash_words_consumed_match_c_oracle(K):
+    for (n, w, s, seed) in [(10_000, 400, 1, 11), (3_000, 400, 18, 14), (1_000, 40, 4, 17)]:
+        k0, k1 = chash.philox_key(seed)
+        _, _, used = K.sparse_embedding(k0, k1, n, w, s)
+        _, _, used_c = chash.sparse_embedding(n, w, s, seed)
+        assert used == used_c
+
+
+def test_hash_full_size_checksums(K):
+    with open(os.path.join(GOLDEN, "hashes_big.json")) as f:
+        big = json.load(f)
+    for case in big["big"]:
+        k0, k1 = chash.philox_key(case["seed"])
+        cols, vals, _ = K.sparse_embedding(k0, k1, case["n"], case["w"], case["s"])
+        c = _h(cols).astype(np.int64)
+        assert _sha(c) == case["cols_sha256"], case
+        assert _sha((_h(vals) > 0).astype(np.int8)) == case["sign_sha256"]
+
+
+def test_lemire_draws_with_rejections(K):
+    g = np.load(os.path.join(GOLDEN, "hashes.npz"))
+    for w in (3 * 2**30, 2**31 + 1, 5):
+        k0, k1 = chash.philox_key(21)
+        out, used = K.lemire_draw(k0, k1, w, 4000)
+        assert np.array_equal(_h(out), g[f"lemire_{w}"])
+        _, used_c = chash.lemire_draw(21, w, 4000)
+        assert used == used_c
+
+
+# ---------------------------------------------------------- column streams
+
+SHAPES = [(1, 7), (20, 600), (63, 1000), (100, 10_000), (257, 3000), (1000, 5000),
+          (1001, 4001), (2000, 3000)]
+
+
+def _problem(m, n, seed=0):
+    g = np.random.Generator(np.random.Philox(seed))
+    A = g.standard_normal((m, n))
+    return g, A
+
+
+@pytest.mark.parametrize("m,n", SHAPES)
+def test_normal_apply(K, m, n):
+    g, A = _problem(m, n)
+    d = 10.0 ** g.uniform(-2, 2, n)
+    z = g.standard_normal(m)
+    Ad = K.DeviceMatrix.from_host(A)
+    d2 = d**2
+    out = torch.empty(m, dtype=torch.float64, device="cuda")
+    K.normal_apply(Ad, _t(d2), _t(z), out)
+    ref = O.NormalOp(sp.csr_matrix(A), d).apply(z)
+    scale = np.abs(A).dot(d2 * np.abs(A.T @ z)).max() + 1e-300
+    assert np.max(np.abs(_h(out) - ref)) <= 1e-13 * scale
+    # deterministic run to run
+    out2 = torch.empty_like(out)
+    K.normal_apply(Ad, _t(d2), _t(z), out2, sub=_t(ref))
+    assert np.array_equal(_h(out2), _h(out) - ref)
+
+
+@pytest.mark.parametrize("m,n", SHAPES)
+def test_gemv_and_transpose(K, m, n):
+    g, A = _problem(m, n, 1)
+    x, y, s, c = g.standard_normal(n), g.standard_normal(m), g.random(n) + 0.5, g.standard_normal(n)
+    b = g.standard_normal(m)
+    Ad = K.DeviceMatrix.from_host(A)
+    u = torch.empty(m, dtype=torch.float64, device="cuda")
+    K.gemv(Ad, _t(x), u, sub=_t(b))
+    ref = A @ x - b
+    assert np.max(np.abs(_h(u) - ref)) <= 1e-13 * (np.abs(A) @ np.abs(x)).max()
+    t = torch.empty(n, dtype=torch.float64, device="cuda")
+    K.gemv_t(Ad, _t(y), t, add=_t(s), sub=_t(c))
+    ref = A.T @ y + s - c
+    assert np.max(np.abs(_h(t) - ref)) <= 1e-13 * (np.abs(A.T) @ np.abs(y) + 1).max()
+    K.gemv_ratio(Ad, _t(x), _t(s), u)
+    ref = A @ (x / s)
+    assert np.max(np.abs(_h(u) - ref)) <= 1e-13 * (np.abs(A) @ np.abs(x / s)).max()
+
+
+@pytest.mark.parametrize("mode", ["feasible", "infeasible"])
+def test_rhs_directions_iterate(K, mode):
+    m, n = 300, 4000
+    g, A = _problem(m, n, 2)
+    x, s = g.random(n) + 0.2, g.random(n) + 0.2
+    y, dy = g.standard_normal(m), g.standard_normal(m)
+    v = 1e-3 * g.standard_normal(n)
+    r_d = 1e-2 * g.standard_normal(n) if mode == "infeasible" else None
+    r_p = 1e-2 * g.standard_normal(m) if mode == "infeasible" else None
+    b, c = g.standard_normal(m), g.standard_normal(n)
+    smu = 0.5 * 0.37
+    Acsr = sp.csr_matrix(A)
+    Ad = K.DeviceMatrix.from_host(A)
+    it = O.Iterate(x, y, s, r_p if r_p is not None else np.zeros(m),
+                   r_d if r_d is not None else np.zeros(n), 0.37)
+    p = torch.empty(m, dtype=torch.float64, device="cuda")
+    K.rhs(Ad, _t(x), _t(s), smu, p, r_d=None if r_d is None else _t(r_d),
+          r_p=None if r_p is None else _t(r_p))
+    ref = O.build_rhs(Acsr, it, 0.5, mode)
+    assert np.max(np.abs(_h(p) - ref)) <= 1e-12 * np.abs(ref).max()
+
+    ds, dx, adx, atdy = (torch.empty(n, dtype=torch.float64, device="cuda"),
+                         torch.empty(n, dtype=torch.float64, device="cuda"),
+                         torch.empty(m, dtype=torch.float64, device="cuda"),
+                         torch.empty(n, dtype=torch.float64, device="cuda"))
+    K.directions(Ad, _t(dy), _t(x), _t(s), _t(v), smu, ds, dx, adx, atdy=atdy,
+                 r_d=None if r_d is None else _t(r_d))
+    Atdy = A.T @ dy
+    ds_ref = -Atdy if mode == "feasible" else -r_d - Atdy
+    dx_ref = -x + smu / s - (x / s) * ds_ref - v / s
+    assert np.max(np.abs(_h(atdy) - Atdy)) <= 1e-13 * np.abs(Atdy).max()
+    assert np.max(np.abs(_h(ds) - ds_ref)) <= 1e-13 * np.abs(ds_ref).max()
+    assert np.max(np.abs(_h(dx) - dx_ref)) <= 1e-12 * np.abs(dx_ref).max()
+    # elementwise formulas are bit-exact given the same A'dy
+    ds_from = -_h(atdy) if mode == "feasible" else -r_d - _h(atdy)
+    assert np.array_equal(_h(ds), ds_from)
+    assert np.array_equal(_h(dx), -x + smu / s - (x / s) * ds_from - v / s)
+    adx_ref = A @ _h(dx)
+    assert np.max(np.abs(_h(adx) - adx_ref)) <= 1e-13 * (np.abs(A) @ np.abs(_h(dx))).max()
+
+    alpha = 0.61
+    xo, so = torch.empty_like(ds), torch.empty_like(ds)
+    rp, rd = torch.empty_like(adx), torch.empty_like(ds)
+    ynew = y + alpha * dy
+    K.iterate(Ad, _t(x), _t(s), _t(ynew), _t(b), _t(c), rp, rd, dx=dx, ds=ds, alpha=alpha,
+              x_out=xo, s_out=so)
+    xn, sn = x + alpha * _h(dx), s + alpha * _h(ds)
+    assert np.array_equal(_h(xo), xn) and np.array_equal(_h(so), sn)
+    ref_rp, ref_rd = A @ xn - b, A.T @ ynew + sn - c
+    assert np.max(np.abs(_h(rp) - ref_rp)) <= 1e-13 * (np.abs(A) @ np.abs(xn)).max()
+    assert np.max(np.abs(_h(rd) - ref_rd)) <= 1e-13 * (np.abs(A.T) @ np.abs(ynew) + 1).max()
