@@ -63,10 +63,18 @@ int skb_lemire_draw(uint64_t key0, uint64_t key1, uint64_t word_offset, uint32_t
  * after the sum. Workspace: skb_stream_workspace_bytes(m). */
 size_t skb_stream_workspace_bytes(int64_t m);
 
-/* u = A (d2 .* (A' z)) [- sub]      NormalOperator.apply (krylov_solvers.py:46-47) */
+/* u = A (d2 .* (A' z)) [- sub]      NormalOperator.apply (krylov_solvers.py:46-47).
+ * gate (nullable device int): when *gate != 0 the launches are no-ops (PCG stopped). */
 int skb_normal_apply(const double* A, int64_t m, int64_t n, int64_t lda, const double* d2,
-                     const double* z, double* u, const double* sub, void* workspace,
-                     size_t ws_bytes, void* stream);
+                     const double* z, double* u, const double* sub, const int* gate,
+                     void* workspace, size_t ws_bytes, void* stream);
+
+/* The streaming pass of skb_normal_apply alone: per-CTA partial m-vectors into
+ * part (>= skb_stream_workspace_bytes(m)); *nparts_host receives their count.
+ * Reduce with skb_reduce_partials. (Used for per-kernel roofline timing.) */
+int skb_normal_apply_partials(const double* A, int64_t m, int64_t n, int64_t lda,
+                              const double* d2, const double* z, double* part,
+                              int32_t* nparts_host, void* stream);
 
 /* u = A x [- sub]                    lp.A @ x (ipm_core.py:99) */
 int skb_gemv(const double* A, int64_t m, int64_t n, int64_t lda, const double* x, double* u,
@@ -107,6 +115,120 @@ int skb_iterate(const double* A, int64_t m, int64_t n, int64_t lda, const double
 /* out = sum_b part[b*m:(b+1)*m] (fixed order) [- sub]. */
 int skb_reduce_partials(const double* part, int32_t nparts, int64_t m, const double* sub,
                         double* out, void* stream);
+
+/* ------------------------------------------------------------ K2 sketch --
+ * X = (A diag(d) W)' for the sparse-sign W given by cols/vals (n x s), i.e.
+ * X[b*ldx + i] = ADW[i, b] (bucket-major, w rows of length m). Bit-exact with
+ * apply_sketch (sketching.py:142-161): per (i, b) the terms fl(fl(A_ij d_j) v)
+ * are added in ascending j without FMA. m <= 2048, w*4 bytes <= 220 KB.
+ * Workspace: skb_sketch_workspace_bytes(n, w, s). */
+size_t skb_sketch_workspace_bytes(int64_t n, int32_t w, int32_t s);
+int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda, const double* d,
+                     const int32_t* cols, const double* vals, int32_t s, int32_t w, double* X,
+                     int64_t ldx, void* workspace, size_t ws_bytes, void* stream);
+
+/* Identity sketch (w >= n, sketching.py:155-156): X[j*ldx + i] = A_ij * d_j. */
+int skb_scale_columns(const double* A, int64_t m, int64_t n, int64_t lda, const double* d,
+                      double* X, int64_t ldx, void* stream);
+
+/* v_j = [sqrt(x_j s_j) *] sum_k vals[j,k] u[cols[j,k]]  (SketchOperator.matvec,
+ * sketching.py:72-80; compute_v, correction.py:58). x == NULL: W u only. */
+int skb_sketch_gather(const int32_t* cols, const double* vals, int32_t s, int64_t n,
+                      const double* u, const double* x, const double* sv, double* v,
+                      void* stream);
+
+/* ------------------------------------------------------- K3 factor (FP64) --
+ * Replaces np.linalg.svd(ADW) (preconditioning.py:46). Factor matrices are
+ * Mp x Mp row-major (Mp = skb_factor_padded_dim(m), identity-padded).
+ * skb_factor_cholqr2: Q = X'X = L L' by CholeskyQR2 (shifted CholeskyQR3 when
+ * the first Gram Cholesky breaks down). Outputs Linv = L^-1 (lower), LinvT
+ * (upper), Lfac = L. stats_host[4] = {min|L_ii|, max|L_ii|, shifted, status}.
+ * Synchronises the stream. Workspace: skb_factor_workspace_bytes(m, w). */
+int32_t skb_factor_padded_dim(int32_t m);
+size_t skb_factor_workspace_bytes(int32_t m, int32_t w);
+int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32_t m, double* Linv,
+                       double* LinvT, double* Lfac, double* stats_host, void* workspace,
+                       size_t ws_bytes, void* stream);
+
+/* C = alpha op(A) op(B) + beta C (row-major, FP64 DMMA tensor cores, batched). */
+int skb_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, double alpha,
+             const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+             int64_t ldc, int32_t lower_only, int32_t batch, int64_t strideA, int64_t strideB,
+             int64_t strideC, void* workspace, size_t ws_bytes, void* stream);
+
+/* Blocked Cholesky (lower, in place) and triangular inverse; Mp % 64 == 0
+ * (power of two for skb_trtri). status: device int, SKB_ST_CHOL_FAIL on a
+ * nonpositive pivot. */
+int skb_potrf(double* G, int64_t ld, int32_t Mp, int* status, void* workspace, size_t ws_bytes,
+              void* stream);
+int skb_trtri(const double* L, double* Li, int64_t ld, int32_t Mp, void* workspace,
+              size_t ws_bytes, void* stream);
+
+/* y = M x, M row-major rows x cols; tri 0 full, 1 lower (k <= i), 2 upper (k >= i).
+ * apply_inv = two calls (Linv then LinvT); apply_pinv_adw = one full call on X. */
+int skb_rowdot_gemv(const double* M, int64_t ld, int32_t rows, int32_t cols, int32_t tri,
+                    const double* x, double* y, const int* gate, void* stream);
+
+/* ------------------------------------------------------------- K6 PCG --
+ * pcg (krylov_solvers.py:65-105) with M^-1 = Linv' Linv. state: device buffer
+ * of skb_pcg_state_bytes(); trace: device (t_max+1) doubles. The step kernels
+ * are gated on the state so a fixed launch sequence can run after convergence
+ * (multi-GPU drivers interleave NCCL allreduces between them). */
+size_t skb_pcg_state_bytes(void);
+int skb_pcg_init(const double* p, double* r, double* dy, int64_t m, void* state, void* stream);
+int skb_pcg_init2(const double* r, const double* z, double* q, int64_t m, double tol, void* state,
+                  double* trace, void* stream);
+int skb_pcg_step_a(const double* q, const double* Aq, double* dy, double* r, int64_t m,
+                   void* state, void* stream);
+int skb_pcg_step_b(const double* r, const double* z, double* q, int64_t m, int32_t t_max,
+                   void* state, double* trace, void* stream);
+
+/* Whole single-device PCG, one synchronisation. vec: 5*ldv doubles scratch.
+ * out_host = {iterations, converged, status bits}; trace_host: iterations+1. */
+int skb_pcg_solve(const double* A, int64_t m, int64_t n, int64_t lda, const double* d2,
+                  const double* Linv, const double* LinvT, int64_t ld, const double* p,
+                  double* dy, double* vec, int64_t ldv, int32_t t_max, double tol, void* state,
+                  double* trace, double* trace_host, int32_t* out_host, void* workspace,
+                  size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------- K8 step reductions --
+ * Deterministic fused elementwise + reduction passes (one launch each; the
+ * results land in the device array `out`). The reduction workspace
+ * (skb_reduce_workspace_bytes) holds a ticket word that must start at zero
+ * (skb_reduce_workspace_init) and must not be shared with other scratch. */
+size_t skb_reduce_workspace_bytes(void);
+int skb_reduce_workspace_init(void* workspace, void* stream);
+
+/* d = sqrt(clip(x/s, 1e-32, 1e32)), d2 = d*d (ipm_core.py:415-421, krylov_solvers.py:40);
+ * out = {clip_count, min x, min s}. */
+int skb_step_prep(const double* x, const double* s, int64_t n, double* d, double* d2,
+                  double* out, void* workspace, size_t ws_bytes, void* stream);
+
+/* out = {sum x.s, min x.s, min x, min s, ||r_d||^2}  (duality_measure / in_neighborhood). */
+int skb_iter_stats(const double* x, const double* s, const double* r_d, int64_t n, double* out,
+                   void* workspace, size_t ws_bytes, void* stream);
+
+/* out = {max|comp|, max|x s|, max|x ds|, max|s dx|, dx'ds, ||dx||^2, sum(x ds + s dx),
+ *        x'ds, s'dx, sum v} with comp = x ds + s dx + x s - sigma_mu + v
+ * (assemble_directions ipm_core.py:237-242, max_alpha :286-289, argmin :328, v_bar :524). */
+int skb_dir_stats(const double* x, const double* s, const double* dx, const double* ds,
+                  const double* v, double sigma_mu, int64_t n, double* out, void* workspace,
+                  size_t ws_bytes, void* stream);
+
+/* Vectorised _first_crossing (ipm_core.py:245-275) for max_alpha's proximity
+ * quadratics: a = dx ds - g1a, b = x ds + s dx - g1b, c = x s - g1mu.
+ * out = {min c, max|c|, crossing with c clamped at 0 (inf if none)}. */
+int skb_crossing(const double* x, const double* s, const double* dx, const double* ds, double g1a,
+                 double g1b, double g1mu, int64_t n, double* out, void* workspace,
+                 size_t ws_bytes, void* stream);
+
+/* out = {sum t^2, sum t, max|t|, min t} for t = a [- sub]. */
+int skb_vec_stats(const double* a, const double* sub, int64_t n, double* out, void* workspace,
+                  size_t ws_bytes, void* stream);
+
+/* y = x + alpha d;  out = a - b. */
+int skb_axpy(const double* x, double alpha, const double* d, double* y, int64_t n, void* stream);
+int skb_sub(const double* a, const double* b, double* out, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,650 @@
+// K3/K5/K7: the sketched preconditioner on device, FP64 throughout.
+//
+// Replaces build_preconditioner's thin SVD (reference preconditioning.py:38-51,
+// LAPACK gesdd) and its applications apply_inv / apply_pinv_adw (:59-66).
+// With X = (ADW)' (w x m, stored bucket-major by skb_sketch_apply):
+//   CholeskyQR2   G1 = X'X = L1 L1',  Y = X L1^-T,  G2 = Y'Y = L2 L2',
+//                 L = L1 L2  (so Q = ADW ADW' = X'X = L L'),  Linv = L2^-1 L1^-1
+//   Q^-1 r      = Linv' (Linv r)                      two triangular gemvs
+//   (ADW)^+ r   = ADW' Q^-1 r = X Q^-1 r              (full row rank)
+// CholeskyQR2 recovers R to QR accuracy where one Gram Cholesky squares the
+// conditioning. A failed first Cholesky (kappa(ADW) ~> 1e8)
+// is retried with the shifted CholeskyQR3 of Fukaya et al.
+//
+// GEMM-class work runs on the FP64 tensor pipe through warp-level
+// mma.sync.aligned.m8n8k4 f64 (SASS DMMA): sm_100a has no tcgen05 kind for
+// FP64. Everything else here is latency- or HBM-bound.
+#include <algorithm>
+#include <cmath>
+
+#include "skb_common.cuh"
+#include "skb_internal.h"
+
+namespace skb {
+
+// ------------------------------------------------------------------ DMMA GEMM
+// C[M][N] = alpha * sum_k opA(i,k) opB(k,j) + beta * C, all row-major.
+// opA(i,k) = TA ? A[k*lda+i] : A[i*lda+k];  opB(k,j) = TB ? B[j*ldb+k] : B[k*ldb+j].
+// Tile 64x64x16, 4 warps (2x2), warp tile 32x32 = 4x4 m8n8k4 fragments.
+// lower_only: skip tiles strictly above the diagonal (symmetric / triangular C).
+// Split-K: blockIdx.z = batch * splits + split; split partials go to `part`
+// and are summed in split order by gemm_splitk_reduce (deterministic).
+constexpr int GBM = 64, GBN = 64, GBK = 16, GPAD = 8;
+
+struct GemmArgs {
+  const double* A;
+  const double* B;
+  double* C;
+  double* part;  // split-K partial buffer (nullptr when splits == 1)
+  int64_t lda, ldb, ldc;
+  int64_t sA, sB, sC;  // batch strides
+  int M, N, K;
+  int splits, kchunk;
+  double alpha, beta;
+  int ta, tb, lower_only;
+};
+
+SKB_DEV void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) dgemm_kernel(GemmArgs g) {
+  __shared__ double As[2][GBK][GBM + GPAD];
+  __shared__ double Bs[2][GBK][GBN + GPAD];
+  const int batch = blockIdx.z / g.splits, split = blockIdx.z % g.splits;
+  const int bm = blockIdx.y, bn = blockIdx.x;
+  if (g.lower_only && bn * GBN > bm * GBM + GBM - 1) return;
+  const int i0 = bm * GBM, j0 = bn * GBN;
+  const double* A = g.A + (int64_t)batch * g.sA;
+  const double* B = g.B + (int64_t)batch * g.sB;
+  const int k_begin = split * g.kchunk, k_end = min(g.K, k_begin + g.kchunk);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  double ra[8], rb[8];
+  // element e of this thread's tile load: tile index t = tid + 128*e in [0, 1024)
+  auto load_tiles = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int t = tid + 128 * e;
+      int kk, ii;
+      if (g.ta) {
+        kk = t >> 6;
+        ii = t & 63;
+      } else {
+        ii = t >> 4;
+        kk = t & 15;
+      }
+      const int gi = i0 + ii, gk = k0 + kk;
+      double v = 0.0;
+      if (gi < g.M && gk < k_end) v = g.ta ? A[(int64_t)gk * g.lda + gi] : A[(int64_t)gi * g.lda + gk];
+      ra[e] = v;
+      int kb, jj;
+      if (g.tb) {
+        jj = t >> 4;
+        kb = t & 15;
+      } else {
+        kb = t >> 6;
+        jj = t & 63;
+      }
+      const int gj = j0 + jj, gk2 = k0 + kb;
+      double u = 0.0;
+      if (gj < g.N && gk2 < k_end)
+        u = g.tb ? B[(int64_t)gj * g.ldb + gk2] : B[(int64_t)gk2 * g.ldb + gj];
+      rb[e] = u;
+    }
+  };
+  auto store_tiles = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int t = tid + 128 * e;
+      if (g.ta)
+        As[buf][t >> 6][t & 63] = ra[e];
+      else
+        As[buf][t & 15][t >> 4] = ra[e];
+      if (g.tb)
+        Bs[buf][t & 15][t >> 4] = rb[e];
+      else
+        Bs[buf][t >> 6][t & 63] = rb[e];
+    }
+  };
+
+  int buf = 0;
+  if (k_begin < k_end) {
+    load_tiles(k_begin);
+    store_tiles(0);
+  }
+  __syncthreads();
+  for (int k0 = k_begin; k0 < k_end; k0 += GBK) {
+    const bool more = k0 + GBK < k_end;
+    if (more) load_tiles(k0 + GBK);
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) af[a] = As[buf][kk + tq][wm + a * 8 + gq];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = Bs[buf][kk + tq][wn + b * 8 + gq];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(acc[a][b], af[a], bf[b]);
+    }
+    if (more) {
+      store_tiles(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+  // epilogue
+  const bool direct = g.splits == 1;
+  double* C = direct ? g.C + (int64_t)batch * g.sC
+                     : g.part + ((int64_t)blockIdx.z) * (int64_t)g.M * g.N;
+  const int64_t ldc = direct ? g.ldc : g.N;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = i0 + wm + a * 8 + gq, j = j0 + wn + b * 8 + tq * 2 + q;
+        if (i < g.M && j < g.N) {
+          double* dst = C + (int64_t)i * ldc + j;
+          if (direct) {
+            double v = g.alpha * acc[a][b][q];
+            if (g.beta != 0.0) v = fma(g.beta, *dst, v);
+            *dst = v;
+          } else {
+            *dst = acc[a][b][q];
+          }
+        }
+      }
+}
+
+__global__ void gemm_splitk_reduce_kernel(GemmArgs g, int nbatch) {
+  const int64_t MN = (int64_t)g.M * g.N;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= MN * nbatch) return;
+  const int batch = (int)(idx / MN);
+  const int64_t r = idx - (int64_t)batch * MN;
+  const int i = (int)(r / g.N), j = (int)(r - (int64_t)i * g.N);
+  if (g.lower_only && j > i) return;
+  double s = 0.0;
+  for (int q = 0; q < g.splits; ++q) s += g.part[((int64_t)batch * g.splits + q) * MN + r];
+  double* dst = g.C + (int64_t)batch * g.sC + (int64_t)i * g.ldc + j;
+  double v = g.alpha * s;
+  if (g.beta != 0.0) v = fma(g.beta, *dst, v);
+  *dst = v;
+}
+
+// ----------------------------------------------------------------- Cholesky
+constexpr int NB = 64;
+
+// Unblocked Cholesky of the nb x nb diagonal block at (k0, k0) (lower, in place).
+__global__ void __launch_bounds__(256) potrf_diag_kernel(double* G, int64_t ld, int k0, int nb,
+                                                          int* status) {
+  __shared__ double a[NB][NB + 1];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  for (int t = tid; t < nb * nb; t += blockDim.x) {
+    const int i = t / nb, j = t % nb;
+    a[i][j] = G[(int64_t)(k0 + i) * ld + k0 + j];
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int c = 0; c < nb; ++c) {
+    if (tid == 0) {
+      const double piv = a[c][c];
+      if (!(piv > 0.0)) bad = 1;
+      a[c][c] = sqrt(piv);
+    }
+    __syncthreads();
+    if (bad) break;
+    const double l = a[c][c];
+    for (int i = c + 1 + tid; i < nb; i += blockDim.x) a[i][c] = a[i][c] / l;
+    __syncthreads();
+    const int rem = nb - c - 1;
+    for (int t = tid; t < rem * rem; t += blockDim.x) {
+      const int i = c + 1 + t / rem, j = c + 1 + t % rem;
+      if (j <= i) a[i][j] -= a[i][c] * a[j][c];
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) atomicOr(status, ST_CHOL_FAIL);
+    return;
+  }
+  for (int t = tid; t < nb * nb; t += blockDim.x) {
+    const int i = t / nb, j = t % nb;
+    G[(int64_t)(k0 + i) * ld + k0 + j] = j <= i ? a[i][j] : 0.0;
+  }
+}
+
+// Panel: rows i in [k0+nb, M) of columns [k0, k0+nb): x L11' = a.
+__global__ void __launch_bounds__(128) trsm_panel_kernel(double* G, int64_t ld, int k0, int nb,
+                                                          int M) {
+  __shared__ double l[NB][NB + 1];
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    const int i = t / nb, j = t % nb;
+    l[i][j] = G[(int64_t)(k0 + i) * ld + k0 + j];
+  }
+  __syncthreads();
+  const int i = k0 + nb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  double* row = G + (int64_t)i * ld + k0;
+  double x[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) x[c] = c < nb ? row[c] : 0.0;
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    if (c < nb) {
+      double t = x[c];
+#pragma unroll
+      for (int q = 0; q < c; ++q) t -= x[q] * l[c][q];
+      x[c] = t / l[c][c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+    if (c < nb) row[c] = x[c];
+}
+
+// Inverse of each 64x64 lower-triangular diagonal block: Linv[b] = L[b]^-1.
+__global__ void __launch_bounds__(64) trtri_diag_kernel(const double* L, double* Li, int64_t ld) {
+  __shared__ double l[NB][NB + 1];
+  const int b0 = blockIdx.x * NB;
+  for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
+    const int i = t / NB, j = t % NB;
+    l[i][j] = L[(int64_t)(b0 + i) * ld + b0 + j];
+  }
+  __syncthreads();
+  const int j = threadIdx.x;  // column of the inverse
+  double x[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    double t = (i == j) ? 1.0 : 0.0;
+    if (i < j) {
+      x[i] = 0.0;
+      continue;
+    }
+#pragma unroll
+    for (int q = 0; q < i; ++q)
+      if (q >= j) t -= l[i][q] * x[q];
+    x[i] = t / l[i][i];
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) Li[(int64_t)(b0 + i) * ld + b0 + j] = x[i];
+}
+
+__global__ void set_identity_pad_kernel(double* G, int64_t ld, int m, int Mp) {
+  // zero rows/cols >= m, unit diagonal there
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)Mp * Mp) return;
+  const int i = (int)(idx / Mp), j = (int)(idx % Mp);
+  if (i >= m || j >= m) G[(int64_t)i * ld + j] = (i == j) ? 1.0 : 0.0;
+}
+
+__global__ void zero_upper_kernel(double* G, int64_t ld, int Mp) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)Mp * Mp) return;
+  const int i = (int)(idx / Mp), j = (int)(idx % Mp);
+  if (j > i) G[(int64_t)i * ld + j] = 0.0;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ S, double* __restrict__ D, int64_t ld,
+                                 int n) {
+  __shared__ double t[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = by + r, j = bx + threadIdx.x;
+    if (i < n && j < n) t[r][threadIdx.x] = S[(int64_t)i * ld + j];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = bx + r, j = by + threadIdx.x;
+    if (i < n && j < n) D[(int64_t)i * ld + j] = t[threadIdx.x][r];
+  }
+}
+
+__global__ void add_diag_kernel(double* G, int64_t ld, int m, double shift) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) G[(int64_t)i * ld + i] += shift;
+}
+
+// stats[0] = trace(G) (= ||X||_F^2), stats[1] = min |L_ii|, stats[2] = max |L_ii|
+__global__ void diag_stats_kernel(const double* G, int64_t ld, int m, double* out, int which) {
+  __shared__ double buf[32];
+  double s = 0.0, mn = INFINITY, mx = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double v = G[(int64_t)i * ld + i];
+    s += v;
+    mn = fmin(mn, fabs(v));
+    mx = fmax(mx, fabs(v));
+  }
+  const double ts = block_sum(s, buf);
+  mn = warp_min(mn);
+  mx = warp_max(mx);
+  __shared__ double smn[32], smx[32];
+  if ((threadIdx.x & 31) == 0) {
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mn = fmin(mn, smn[w]);
+      mx = fmax(mx, smx[w]);
+    }
+    if (which == 0)
+      out[0] = ts;
+    else {
+      out[1] = mn;
+      out[2] = mx;
+    }
+  }
+}
+
+// ------------------------------------------------------------ row-dot gemv
+// y[i] = sum_k M[i][k] x[k] over k in [lo(i), hi(i)); tri = 0 full, 1 lower (k<=i), 2 upper (k>=i).
+// Warp per row. Optional: y = alpha*y... kept plain; scal (nullable) divides by scal[i].
+__global__ void __launch_bounds__(256) rowdot_gemv_kernel(const double* __restrict__ Mx,
+                                                          int64_t ld, int rows, int cols, int tri,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y,
+                                                          const int* __restrict__ gate) {
+  if (gate && *gate) return;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int i = warp;
+  const int lo = tri == 2 ? i : 0, hi = tri == 1 ? min(i + 1, cols) : cols;
+  const double* row = Mx + (int64_t)i * ld;
+  double s0 = 0.0, s1 = 0.0;
+  int k = lo + lane;
+  for (; k + 32 < hi; k += 64) {
+    s0 = fma(row[k], x[k], s0);
+    s1 = fma(row[k + 32], x[k + 32], s1);
+  }
+  if (k < hi) s0 = fma(row[k], x[k], s0);
+  const double s = warp_sum(s0 + s1);
+  if (lane == 0) y[i] = s;
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+// ----------------------------------------------------------------- host API
+
+static int gemm_launch(const GemmArgs& base, int nbatch, skb_ws* ws, cudaStream_t st) {
+  GemmArgs g = base;
+  if (g.M <= 0 || g.N <= 0) return 0;
+  const int tm = (g.M + GBM - 1) / GBM, tn = (g.N + GBN - 1) / GBN;
+  int tiles = tm * tn * nbatch;
+  if (g.lower_only) tiles = (tiles + 1) / 2;
+  const int target = 2 * skb_num_sms();
+  int splits = 1;
+  if (g.K > 256 && tiles < target) {
+    splits = std::min((target + tiles - 1) / tiles, std::max(1, g.K / 256));
+    splits = std::max(1, std::min(splits, 64));
+    // bound the partial buffer by the remaining workspace
+    const size_t per = (size_t)nbatch * g.M * g.N * 8;
+    const size_t avail = ws->cap > ws->off + 512 ? ws->cap - ws->off - 512 : 0;
+    while (splits > 1 && per * splits > avail) --splits;
+  }
+  g.splits = splits;
+  g.kchunk = (((g.K + splits - 1) / splits) + GBK - 1) / GBK * GBK;
+  g.splits = (g.K + g.kchunk - 1) / g.kchunk;
+  if (g.splits < 1) g.splits = 1;
+  g.part = nullptr;
+  const size_t mark = ws->off;
+  if (g.splits > 1) {
+    g.part = (double*)skb_ws_take(ws, (size_t)nbatch * g.splits * g.M * g.N * 8);
+    if (!g.part) {  // fall back to no split
+      g.splits = 1;
+      g.kchunk = std::max(g.K, 1);
+    }
+  }
+  if (g.K <= 0) g.kchunk = 1;
+  dim3 grid(tn, tm, nbatch * g.splits);
+  dgemm_kernel<<<grid, 128, 0, st>>>(g);
+  if (g.splits > 1) {
+    const int64_t tot = (int64_t)g.M * g.N * nbatch;
+    gemm_splitk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g, nbatch);
+  }
+  ws->off = mark;
+  return skb_launch_status(__func__);
+}
+
+static GemmArgs gemm_args(const double* A, int64_t lda, int ta, const double* B, int64_t ldb,
+                          int tb, double* C, int64_t ldc, int M, int N, int K, double alpha,
+                          double beta, int lower_only) {
+  GemmArgs g{};
+  g.A = A;
+  g.B = B;
+  g.C = C;
+  g.lda = lda;
+  g.ldb = ldb;
+  g.ldc = ldc;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.ta = ta;
+  g.tb = tb;
+  g.lower_only = lower_only;
+  g.splits = 1;
+  return g;
+}
+
+extern "C" int skb_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, double alpha,
+                        const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                        double* C, int64_t ldc, int32_t lower_only, int32_t batch, int64_t strideA,
+                        int64_t strideB, int64_t strideC, void* workspace, size_t ws_bytes,
+                        void* stream) {
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  GemmArgs g = gemm_args(A, lda, ta, B, ldb, tb, C, ldc, M, N, K, alpha, beta, lower_only);
+  g.sA = strideA;
+  g.sB = strideB;
+  g.sC = strideC;
+  return gemm_launch(g, std::max(1, batch), &ws, (cudaStream_t)stream);
+}
+
+static int round_pad(int m) {
+  int p = NB;
+  while (p < m) p <<= 1;
+  return p;
+}
+
+extern "C" int32_t skb_factor_padded_dim(int32_t m) { return round_pad(m); }
+
+// Blocked right-looking Cholesky of the (Mp x Mp, ld) lower part in place.
+static int potrf(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStream_t st) {
+  for (int k0 = 0; k0 < Mp; k0 += NB) {
+    potrf_diag_kernel<<<1, 256, 0, st>>>(G, ld, k0, NB, status);
+    const int rest = Mp - k0 - NB;
+    if (rest <= 0) break;
+    trsm_panel_kernel<<<(rest + 127) / 128, 128, 0, st>>>(G, ld, k0, NB, Mp);
+    double* P = G + (int64_t)(k0 + NB) * ld + k0;
+    double* T = G + (int64_t)(k0 + NB) * ld + k0 + NB;
+    GemmArgs g = gemm_args(P, ld, 0, P, ld, 1, T, ld, rest, rest, NB, -1.0, 1.0, 1);
+    int rc = gemm_launch(g, 1, ws, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+extern "C" int skb_potrf(double* G, int64_t ld, int32_t Mp, int* status, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  if (Mp % NB) return SKB_ERR_ARG;
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = potrf(G, ld, Mp, status, &ws, st);
+  if (rc) return rc;
+  zero_upper_kernel<<<(unsigned)(((int64_t)Mp * Mp + 255) / 256), 256, 0, st>>>(G, ld, Mp);
+  return skb_launch_status(__func__);
+}
+
+// Li = L^-1 for lower-triangular L (Mp = 64 * 2^k, ld), by recursive doubling:
+// inv([A 0; B C]) = [A^-1 0; -C^-1 B A^-1  C^-1], all pairs of a level batched.
+static int trtri(const double* L, double* Li, int64_t ld, int Mp, skb_ws* ws, cudaStream_t st) {
+  cudaMemsetAsync(Li, 0, (size_t)Mp * ld * 8, st);
+  trtri_diag_kernel<<<Mp / NB, NB, 0, st>>>(L, Li, ld);
+  const size_t mark = ws->off;
+  double* T = (double*)skb_ws_take(ws, (size_t)Mp * Mp / 2 * 8);
+  if (!T) return SKB_ERR_WORKSPACE;
+  for (int h = NB; h < Mp; h <<= 1) {
+    const int pairs = Mp / (2 * h);
+    const int64_t s = (int64_t)2 * h * (ld + 1);  // diagonal stride between pairs
+    // T_p = L21_p * Li11_p  (h x h each), T stored contiguous h x h per pair
+    GemmArgs g1 = gemm_args(L + (int64_t)h * ld, ld, 0, Li, ld, 0, T, h, h, h, h, 1.0, 0.0, 0);
+    g1.sA = s;
+    g1.sB = s;
+    g1.sC = (int64_t)h * h;
+    int rc = gemm_launch(g1, pairs, ws, st);
+    if (rc) return rc;
+    // Li21_p = -Li22_p * T_p
+    GemmArgs g2 = gemm_args(Li + (int64_t)h * ld + h, ld, 0, T, h, 0, Li + (int64_t)h * ld, ld, h,
+                            h, h, -1.0, 0.0, 0);
+    g2.sA = s;
+    g2.sB = (int64_t)h * h;
+    g2.sC = s;
+    rc = gemm_launch(g2, pairs, ws, st);
+    if (rc) return rc;
+  }
+  ws->off = mark;
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_trtri(const double* L, double* Li, int64_t ld, int32_t Mp, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  if (Mp % NB || (Mp & (Mp - 1))) return SKB_ERR_ARG;
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  return trtri(L, Li, ld, Mp, &ws, (cudaStream_t)stream);
+}
+
+extern "C" size_t skb_factor_workspace_bytes(int32_t m, int32_t w) {
+  const size_t Mp = (size_t)round_pad(m);
+  const size_t ldx = (size_t)(m + (m & 1));
+  // G, L1inv, L2inv, Y + GEMM split partials (<= 64 * 2 * 148 tiles) + trtri temp
+  const size_t split = 4 * Mp * Mp * 8;  // split-K partials
+  return 3 * Mp * Mp * 8 + (size_t)w * ldx * 8 + Mp * Mp * 4 + split + 16 * 256;
+}
+
+// CholeskyQR2 of X' (X: w x m bucket-major, ldx). Outputs (Mp x Mp, ld = Mp):
+// Linv (lower, = L^-1), LinvT (upper, its transpose), Lfac (lower L = L1 L2).
+// stats_host[0..3]: min|L_ii|, max|L_ii| (of L), shifted (0/1), chol status.
+// Synchronises the stream once (to test the first Cholesky).
+extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32_t m,
+                                  double* Linv, double* LinvT, double* Lfac, double* stats_host,
+                                  void* workspace, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < 1 || w < m) return SKB_ERR_ARG;
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  const int Mp = round_pad(m);
+  const int64_t ld = Mp;
+  const size_t MM = (size_t)Mp * Mp;
+  double* G = (double*)skb_ws_take(&ws, MM * 8);
+  double* L1i = (double*)skb_ws_take(&ws, MM * 8);
+  double* L2i = (double*)skb_ws_take(&ws, MM * 8);
+  double* Y = (double*)skb_ws_take(&ws, (size_t)w * ldx * 8);
+  int* status = (int*)skb_ws_take(&ws, 64);
+  double* dstat = (double*)skb_ws_take(&ws, 64);
+  if (!G || !L1i || !L2i || !Y || !status || !dstat) return SKB_ERR_WORKSPACE;
+  const unsigned eb = (unsigned)((MM + 255) / 256);
+  int rc;
+  double hstat[4];
+  int hst = 0;
+  bool shifted = false;
+
+  auto gram = [&](const double* Z) -> int {  // G = Z'Z (lower tiles), identity padding
+    cudaMemsetAsync(G, 0, MM * 8, st);
+    GemmArgs g = gemm_args(Z, ldx, 1, Z, ldx, 0, G, ld, m, m, w, 1.0, 0.0, 1);
+    int r = gemm_launch(g, 1, &ws, st);
+    set_identity_pad_kernel<<<eb, 256, 0, st>>>(G, ld, m, Mp);
+    return r;
+  };
+  // ---- pass 1 (optionally shifted)
+  cudaMemsetAsync(status, 0, 64, st);
+  if ((rc = gram(X))) return rc;
+  diag_stats_kernel<<<1, 1024, 0, st>>>(G, ld, m, dstat, 0);
+  if ((rc = potrf(G, ld, Mp, status, &ws, st))) return rc;
+  cudaMemcpyAsync(&hst, status, 4, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(hstat, dstat, 8, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  if (hst & ST_CHOL_FAIL) {
+    // shifted CholeskyQR: s = 11 (m w + m (m + 1)) u ||X||_F^2
+    shifted = true;
+    const double u = 1.1102230246251565e-16;
+    const double shift = 11.0 * ((double)m * w + (double)m * (m + 1)) * u * hstat[0];
+    cudaMemsetAsync(status, 0, 64, st);
+    if ((rc = gram(X))) return rc;
+    add_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(G, ld, m, shift);
+    if ((rc = potrf(G, ld, Mp, status, &ws, st))) return rc;
+  }
+  zero_upper_kernel<<<eb, 256, 0, st>>>(G, ld, Mp);
+  if ((rc = trtri(G, L1i, ld, Mp, &ws, st))) return rc;
+  cudaMemcpyAsync(Lfac, G, MM * 8, cudaMemcpyDeviceToDevice, st);  // L = L1 (so far)
+
+  const int passes = shifted ? 2 : 1;
+  const double* Z = X;
+  for (int p = 0; p < passes; ++p) {
+    // Y = Z * L1i'  (w x m)
+    GemmArgs gy = gemm_args(Z, ldx, 0, L1i, ld, 1, Y, ldx, w, m, m, 1.0, 0.0, 0);
+    if ((rc = gemm_launch(gy, 1, &ws, st))) return rc;
+    Z = Y;
+    if ((rc = gram(Y))) return rc;
+    if ((rc = potrf(G, ld, Mp, status, &ws, st))) return rc;
+    zero_upper_kernel<<<eb, 256, 0, st>>>(G, ld, Mp);
+    if ((rc = trtri(G, L2i, ld, Mp, &ws, st))) return rc;
+    // Linv = L2i * L1i (lower x lower); Lfac = Lfac * L2 (G holds L2)
+    GemmArgs gi = gemm_args(L2i, ld, 0, L1i, ld, 0, Linv, ld, Mp, Mp, Mp, 1.0, 0.0, 1);
+    if ((rc = gemm_launch(gi, 1, &ws, st))) return rc;
+    zero_upper_kernel<<<eb, 256, 0, st>>>(Linv, ld, Mp);  // skipped tiles hold stale data
+    GemmArgs gl = gemm_args(Lfac, ld, 0, G, ld, 0, L2i /*tmp*/, ld, Mp, Mp, Mp, 1.0, 0.0, 1);
+    if ((rc = gemm_launch(gl, 1, &ws, st))) return rc;
+    zero_upper_kernel<<<eb, 256, 0, st>>>(L2i, ld, Mp);
+    cudaMemcpyAsync(Lfac, L2i, MM * 8, cudaMemcpyDeviceToDevice, st);
+    if (p + 1 < passes) {
+      // next pass factors Y again: L1i <- Linv (cumulative inverse), Y = X Linv'
+      cudaMemcpyAsync(L1i, Linv, MM * 8, cudaMemcpyDeviceToDevice, st);
+      Z = X;
+    }
+  }
+  zero_upper_kernel<<<eb, 256, 0, st>>>(Linv, ld, Mp);
+  zero_upper_kernel<<<eb, 256, 0, st>>>(Lfac, ld, Mp);
+  dim3 tg((Mp + 31) / 32, (Mp + 31) / 32);
+  transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(Linv, LinvT, ld, Mp);
+  diag_stats_kernel<<<1, 1024, 0, st>>>(Lfac, ld, m, dstat, 1);
+  cudaMemcpyAsync(hstat, dstat, 24, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&hst, status, 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  if (stats_host) {
+    stats_host[0] = hstat[1];
+    stats_host[1] = hstat[2];
+    stats_host[2] = shifted ? 1.0 : 0.0;
+    stats_host[3] = (double)hst;
+  }
+  return 0;
+}
+
+// y = M x with M row-major (rows x cols, ld); tri 0 full, 1 lower, 2 upper.
+extern "C" int skb_rowdot_gemv(const double* Mx, int64_t ld, int32_t rows, int32_t cols,
+                               int32_t tri, const double* x, double* y, const int* gate,
+                               void* stream) {
+  if (rows <= 0) return 0;
+  const int64_t threads = (int64_t)rows * 32;
+  rowdot_gemv_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      Mx, ld, rows, cols, tri, x, y, gate);
+  return skb_launch_status(__func__);
+}

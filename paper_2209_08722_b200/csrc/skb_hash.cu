@@ -321,5 +321,5 @@ extern "C" int skb_sparse_embedding(uint64_t key0, uint64_t key1, int64_t n, int
   sign_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(key0, key1, pos, cnt, s, vals);
   pos += (uint64_t)cnt;
   if (words_used) *words_used = pos;
-  return cudaGetLastError() == cudaSuccess ? 0 : SKB_ERR_CUDA;
+  return skb_launch_status(__func__);
 }

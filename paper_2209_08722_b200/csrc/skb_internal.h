@@ -39,3 +39,15 @@ static inline int skb_num_sms() {
   }
   return n;
 }
+
+#include <stdio.h>
+
+// Collect the last launch error; on failure report it on stderr (the C ABI
+// only returns a code) and return SKB_ERR_CUDA.
+static inline int skb_launch_status(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return 0;
+  fprintf(stderr, "[skb] %s: CUDA error %s (%s)\n", where, cudaGetErrorName(e),
+          cudaGetErrorString(e));
+  return SKB_ERR_CUDA;
+}

@@ -1,0 +1,196 @@
+// K6: preconditioned CG on A D^2 A' dy = p with M^-1 = Q^-1 = Linv' Linv.
+//
+// Replaces pcg (reference krylov_solvers.py:65-105). The whole t_max-step
+// recurrence is enqueued without host round trips: scalars live in a device
+// PcgState, and every kernel of an iteration (the fused normal matvec, the
+// m-vector updates, the two triangular gemvs) is gated on state->stop so the
+// launches after convergence or breakdown are no-ops. The host reads the
+// trace once at the end. Vector updates use numpy's rounding order
+// (dy + alpha*q, r - alpha*Aq, z + beta*q) via explicit _rn intrinsics.
+#include "skb_common.cuh"
+#include "skb_internal.h"
+
+namespace skb {
+
+struct PcgState {
+  double gamma, target, norm0, pad;
+  int stop, status, iters, converged;
+};
+
+// r = p, dy = 0
+__global__ void pcg_init_a_kernel(const double* __restrict__ p, double* __restrict__ r,
+                                  double* __restrict__ dy, int m, PcgState* S) {
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    r[i] = p[i];
+    dy[i] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    S->stop = 0;
+    S->status = 0;
+    S->iters = 0;
+    S->converged = 0;
+  }
+}
+
+// gamma = r.z; trace[0] = sqrt(gamma); q = z
+__global__ void pcg_init_b_kernel(const double* __restrict__ r, const double* __restrict__ z,
+                                  double* __restrict__ q, int m, double tol, PcgState* S,
+                                  double* trace) {
+  __shared__ double buf[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) s = fma(r[i], z[i], s);
+  const double g = block_sum(s, buf);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) q[i] = z[i];
+  if (threadIdx.x == 0) {
+    S->gamma = g;
+    if (g < 0.0) {
+      S->status |= ST_BREAKDOWN_RZ;
+      S->stop = 1;
+      return;
+    }
+    const double n0 = sqrt(g);
+    S->norm0 = n0;
+    trace[0] = n0;
+    S->target = tol * n0;
+    if (n0 == 0.0) {
+      S->converged = 1;
+      S->stop = 1;
+    }
+  }
+}
+
+// curv = q.Aq; alpha = gamma/curv; dy += alpha q; r -= alpha Aq
+__global__ void pcg_step_a_kernel(const double* __restrict__ q, const double* __restrict__ Aq,
+                                  double* __restrict__ dy, double* __restrict__ r, int m,
+                                  PcgState* S) {
+  __shared__ double buf[32];
+  if (S->stop) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) s = fma(q[i], Aq[i], s);
+  const double curv = block_sum(s, buf);
+  if (curv <= 0.0 || curv != curv) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      S->status |= ST_BREAKDOWN_CURV;
+      S->stop = 1;
+    }
+    return;
+  }
+  const double alpha = __ddiv_rn(S->gamma, curv);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    dy[i] = __dadd_rn(dy[i], __dmul_rn(alpha, q[i]));
+    r[i] = __dsub_rn(r[i], __dmul_rn(alpha, Aq[i]));
+  }
+}
+
+// gamma' = r.z; trace; convergence; q = z + (gamma'/gamma) q
+__global__ void pcg_step_b_kernel(const double* __restrict__ r, const double* __restrict__ z,
+                                  double* __restrict__ q, int m, int t_max, PcgState* S,
+                                  double* trace) {
+  __shared__ double buf[32];
+  __shared__ int done;
+  if (S->stop) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) s = fma(r[i], z[i], s);
+  const double gn = block_sum(s, buf);
+  if (threadIdx.x == 0) {
+    done = 0;
+    if (gn < 0.0) {
+      S->status |= ST_BREAKDOWN_RZ;
+      S->stop = 1;
+      done = 1;
+    } else {
+      const double nrm = sqrt(gn);
+      const int it = S->iters + 1;
+      trace[it] = nrm;
+      S->iters = it;
+      if (nrm <= S->target) {
+        S->converged = 1;
+        S->stop = 1;
+        done = 1;
+      } else if (it >= t_max) {
+        S->stop = 1;
+        done = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (done) return;
+  const double beta = __ddiv_rn(gn, S->gamma);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) q[i] = __dadd_rn(z[i], __dmul_rn(beta, q[i]));
+  __syncthreads();
+  if (threadIdx.x == 0) S->gamma = gn;
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+extern "C" size_t skb_pcg_state_bytes(void) { return sizeof(PcgState); }
+
+extern "C" int skb_pcg_init(const double* p, double* r, double* dy, int64_t m, void* state,
+                            void* stream) {
+  pcg_init_a_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(p, r, dy, (int)m, (PcgState*)state);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_pcg_init2(const double* r, const double* z, double* q, int64_t m, double tol,
+                             void* state, double* trace, void* stream) {
+  pcg_init_b_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(r, z, q, (int)m, tol,
+                                                          (PcgState*)state, trace);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_pcg_step_a(const double* q, const double* Aq, double* dy, double* r,
+                              int64_t m, void* state, void* stream) {
+  pcg_step_a_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(q, Aq, dy, r, (int)m,
+                                                          (PcgState*)state);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_pcg_step_b(const double* r, const double* z, double* q, int64_t m,
+                              int32_t t_max, void* state, double* trace, void* stream) {
+  pcg_step_b_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(r, z, q, (int)m, t_max,
+                                                          (PcgState*)state, trace);
+  return skb_launch_status(__func__);
+}
+
+// Whole PCG on one device: init, then t_max gated iterations, one sync.
+// Vectors (m each): p in; dy out; r, z, q, Aq, t scratch (pass `vec` = 5*ldv doubles).
+// Linv / LinvT: (ld x ld) lower / upper. out_host[0] = iterations, [1] = converged,
+// [2] = status bits; trace_host receives iterations+1 norms.
+extern "C" int skb_pcg_solve(const double* A, int64_t m, int64_t n, int64_t lda, const double* d2,
+                             const double* Linv, const double* LinvT, int64_t ld,
+                             const double* p, double* dy, double* vec, int64_t ldv,
+                             int32_t t_max, double tol, void* state, double* trace,
+                             double* trace_host, int32_t* out_host, void* workspace,
+                             size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  PcgState* S = (PcgState*)state;
+  double *r = vec, *z = vec + ldv, *q = vec + 2 * ldv, *Aq = vec + 3 * ldv, *t = vec + 4 * ldv;
+  const int* gate = &S->stop;
+  int rc;
+  if ((rc = skb_pcg_init(p, r, dy, m, state, stream))) return rc;
+  if ((rc = skb_rowdot_gemv(Linv, ld, (int)m, (int)m, 1, r, t, nullptr, stream))) return rc;
+  if ((rc = skb_rowdot_gemv(LinvT, ld, (int)m, (int)m, 2, t, z, nullptr, stream))) return rc;
+  if ((rc = skb_pcg_init2(r, z, q, m, tol, state, trace, stream))) return rc;
+  for (int it = 0; it < t_max; ++it) {
+    if ((rc = skb_normal_apply(A, m, n, lda, d2, q, Aq, nullptr, gate, workspace, ws_bytes,
+                               stream)))
+      return rc;
+    if ((rc = skb_pcg_step_a(q, Aq, dy, r, m, state, stream))) return rc;
+    if ((rc = skb_rowdot_gemv(Linv, ld, (int)m, (int)m, 1, r, t, gate, stream))) return rc;
+    if ((rc = skb_rowdot_gemv(LinvT, ld, (int)m, (int)m, 2, t, z, gate, stream))) return rc;
+    if ((rc = skb_pcg_step_b(r, z, q, m, t_max, state, trace, stream))) return rc;
+  }
+  PcgState h;
+  cudaMemcpyAsync(&h, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  if (trace_host && h.iters + 1 > 0) {
+    cudaMemcpy(trace_host, trace, sizeof(double) * (size_t)(h.iters + 1), cudaMemcpyDeviceToHost);
+  }
+  out_host[0] = h.iters;
+  out_host[1] = h.converged;
+  out_host[2] = h.status;
+  return 0;
+}

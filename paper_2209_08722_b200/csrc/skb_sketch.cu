@@ -1,0 +1,352 @@
+// K2: ADW = A diag(d) W for the sparse-sign / CountSketch W, bit-exact.
+//
+// Replaces apply_sketch (reference sketching.py:142-161): AD = A.multiply(d)
+// then (AD @ W_csr).toarray() via scipy csr_matmat, which for every row i and
+// bucket b sums fl(fl(A_ij d_j) v_jk) over the entries (j,k) with cols[j,k] = b
+// in ascending j, one multiply and one add per term, starting from 0.
+//
+// B200 mapping (output stored bucket-major: X[b][i] = ADW[i][b], i.e. ADW'):
+//  1. stable counting sort of the n*s entries by bucket (chunk histograms,
+//     per-chunk exclusive offsets, warp-synchronous match_any ranking) ->
+//     member lists in ascending j;
+//  2. persistent CTAs, one bucket at a time (dynamic fetch): a producer warp
+//     streams the member columns (contiguous, column-major A) through a ring
+//     of shared-memory stages with the TMA bulk engine; 256 consumer threads
+//     each own a pair of rows and accumulate in registers in member order with
+//     __dmul_rn/__dadd_rn (no FMA). Splitting rows (not members) across
+//     threads keeps the per-(i, b) summation order of the reference exactly.
+#include <algorithm>
+
+#include "skb_common.cuh"
+#include "skb_internal.h"
+
+namespace skb {
+
+__global__ void bucket_hist_kernel(const int32_t* __restrict__ cols, int64_t N, int64_t C, int w,
+                                   int32_t* __restrict__ hist) {
+  const int64_t e0 = (int64_t)blockIdx.x * C, e1 = min(N, e0 + C);
+  int32_t* h = hist + (int64_t)blockIdx.x * w;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[cols[e]], 1);
+}
+
+// In place: hist[c][b] <- sum_{c' < c} hist[c'][b]; total[b] <- sum_c hist[c][b].
+__global__ void bucket_chunk_prefix_kernel(int32_t* __restrict__ hist, int nchunks, int w,
+                                           uint32_t* __restrict__ total) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= w) return;
+  int32_t run = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int32_t t = hist[(int64_t)c * w + b];
+    hist[(int64_t)c * w + b] = run;
+    run += t;
+  }
+  total[b] = (uint32_t)run;
+}
+
+// One warp per chunk: entries in ascending order, ranks via match_any.
+__global__ void bucket_scatter_kernel(const int32_t* __restrict__ cols,
+                                      const double* __restrict__ vals, int64_t N, int s,
+                                      int64_t C, int w, const int32_t* __restrict__ hist,
+                                      const uint64_t* __restrict__ start,
+                                      int32_t* __restrict__ mem_j, double* __restrict__ mem_v) {
+  extern __shared__ uint32_t cursor[];
+  const int lane = threadIdx.x;
+  const int64_t c = blockIdx.x, e0 = c * C, e1 = min(N, e0 + C);
+  for (int b = lane; b < w; b += 32) cursor[b] = (uint32_t)(start[b] + hist[c * w + b]);
+  __syncwarp();
+  for (int64_t base = e0; base < e1; base += 32) {
+    const int64_t e = base + lane;
+    const bool act = e < e1;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    if (!act) break;
+    const int b = cols[e];
+    const unsigned peers = __match_any_sync(amask, b);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    const uint32_t pos = cursor[b] + rank;
+    mem_j[pos] = (int32_t)(e / s);
+    mem_v[pos] = vals[e];
+    __syncwarp(amask);
+    if (rank == 0) cursor[b] += __popc(peers);
+    __syncwarp(amask);
+  }
+}
+
+__global__ void scan_buckets_kernel(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
+                                    int n) {
+  __shared__ uint64_t part[1024];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const uint64_t v = i < n ? in[i] : 0;
+    part[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const uint64_t t = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+      __syncthreads();
+      part[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < n) out[i] = carry + part[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += part[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+struct StageMeta {
+  double d, v;
+  int32_t bucket;  // -1: terminate
+  int32_t flags;   // 1 first, 2 last, 4 empty bucket
+};
+
+constexpr int kConsumers = 256;
+
+template <int KP>  // row pairs per consumer thread: m <= 512 * KP
+__global__ void __launch_bounds__(kConsumers + 32, 1)
+    sketch_accumulate_kernel(const double* __restrict__ A, int64_t lda, int m,
+                             const double* __restrict__ d, const uint64_t* __restrict__ start,
+                             const int32_t* __restrict__ mem_j, const double* __restrict__ mem_v,
+                             int w, int stages, unsigned int* __restrict__ counter,
+                             double* __restrict__ X, int64_t ldx) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const size_t col_bytes = (size_t)lda * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + stages;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + stages);
+  size_t off = ((size_t)stages * (16 + sizeof(StageMeta)) + 127) & ~(size_t)127;
+  unsigned char* bufs = smem + off;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // ---------------- producer warp (lane 0 issues, all lanes fetch metadata)
+    const uint64_t pol = l2_evict_first_policy();
+    int st = 0;
+    uint32_t ph = 0;
+    auto next = [&]() {
+      if (++st == stages) {
+        st = 0;
+        ph ^= 1;
+      }
+    };
+    for (;;) {
+      int b = 0;
+      if (lane == 0) b = (int)atomicAdd(counter, 1u);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (b >= w) break;
+      const uint64_t e0 = start[b], e1 = start[b + 1];
+      if (e0 == e1) {
+        if (lane == 0) {
+          mbar_wait(&empty[st], ph ^ 1);
+          meta[st] = StageMeta{0.0, 0.0, b, 1 | 2 | 4};
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[st]))
+                       : "memory");
+        }
+        next();
+        continue;
+      }
+      for (uint64_t eb = e0; eb < e1; eb += 32) {
+        const uint64_t e = eb + lane;
+        int64_t j = 0;
+        double v = 0.0, dj = 0.0;
+        if (e < e1) {
+          j = mem_j[e];
+          v = mem_v[e];
+          dj = d[j];
+        }
+        const int cnt = (int)min((uint64_t)32, e1 - eb);
+        for (int q = 0; q < cnt; ++q) {
+          const int64_t jq = __shfl_sync(0xffffffffu, j, q);
+          const double vq = __shfl_sync(0xffffffffu, v, q);
+          const double dq = __shfl_sync(0xffffffffu, dj, q);
+          if (lane == 0) {
+            const uint64_t eq = eb + q;
+            mbar_wait(&empty[st], ph ^ 1);
+            meta[st] = StageMeta{dq, vq, b, (eq == e0 ? 1 : 0) | (eq + 1 == e1 ? 2 : 0)};
+            mbar_arrive_expect_tx(&full[st], (uint32_t)col_bytes);
+            bulk_g2s(bufs + (size_t)st * col_bytes, A + jq * lda, (uint32_t)col_bytes, &full[st],
+                     pol);
+          }
+          next();
+        }
+      }
+    }
+    if (lane == 0) {
+      mbar_wait(&empty[st], ph ^ 1);
+      meta[st] = StageMeta{0.0, 0.0, -1, 0};
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[st]))
+                   : "memory");
+    }
+    return;
+  }
+
+  // ------------------------------------ consumers: thread p owns row pairs 2p + 512k
+  const int p = threadIdx.x - 32;
+  double2 acc[KP];
+  int st = 0;
+  uint32_t ph = 0;
+  for (;;) {
+    mbar_wait(&full[st], ph);
+    const StageMeta mt = meta[st];
+    if (mt.bucket < 0) break;
+    if (mt.flags & 1) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) acc[k] = make_double2(0.0, 0.0);
+    }
+    if (!(mt.flags & 4)) {
+      const double* col = reinterpret_cast<const double*>(bufs + (size_t)st * col_bytes);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int r = 512 * k + 2 * p;
+        if (r < m) {
+          const double2 a = *reinterpret_cast<const double2*>(col + r);
+          acc[k].x = __dadd_rn(acc[k].x, __dmul_rn(__dmul_rn(a.x, mt.d), mt.v));
+          acc[k].y = __dadd_rn(acc[k].y, __dmul_rn(__dmul_rn(a.y, mt.d), mt.v));
+        }
+      }
+    }
+    if (mt.flags & 2) {
+      double* out = X + (int64_t)mt.bucket * ldx;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int r = 512 * k + 2 * p;
+        if (r + 1 < m)
+          *reinterpret_cast<double2*>(out + r) = acc[k];
+        else if (r < m)
+          out[r] = acc[k].x;
+      }
+    }
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st]))
+                   : "memory");
+    if (++st == stages) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+}
+
+// Identity sketch (w >= n): ADW = AD, X[j][i] = A_ij * d_j  (sketching.py:155-156).
+__global__ void scale_columns_kernel(const double* __restrict__ A, int64_t lda, int m, int64_t n,
+                                     const double* __restrict__ d, double* __restrict__ X,
+                                     int64_t ldx) {
+  const int64_t j = blockIdx.x;
+  if (j >= n) return;
+  const double dj = d[j];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) X[j * ldx + i] = __dmul_rn(A[j * lda + i], dj);
+}
+
+// v_j = sqrt(x_j s_j) * sum_k vals[j,k] u[cols[j,k]]   (correction.py:58; sketching.py:80)
+__global__ void sketch_gather_kernel(const int32_t* __restrict__ cols,
+                                     const double* __restrict__ vals, int s, int64_t n,
+                                     const double* __restrict__ u, const double* __restrict__ x,
+                                     const double* __restrict__ sv, double* __restrict__ v) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double t = __dmul_rn(vals[j * s], u[cols[j * s]]);
+  for (int k = 1; k < s; ++k) t = __dadd_rn(t, __dmul_rn(vals[j * s + k], u[cols[j * s + k]]));
+  if (x) t = __dmul_rn(__dsqrt_rn(__dmul_rn(x[j], sv[j])), t);
+  v[j] = t;
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+extern "C" size_t skb_sketch_workspace_bytes(int64_t n, int32_t w, int32_t s) {
+  const int64_t N = n * (int64_t)s;
+  int64_t C = std::max<int64_t>(4096, (N * (int64_t)w) / (16ll << 20) + 1);
+  const int64_t nch = (N + C - 1) / C;
+  return (size_t)nch * w * 4 + (size_t)w * 4 + (size_t)(w + 1) * 8 + (size_t)N * 12 + 16 + 8 * 256;
+}
+
+extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda,
+                                const double* d, const int32_t* cols, const double* vals,
+                                int32_t s, int32_t w, double* X, int64_t ldx, void* workspace,
+                                size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < 1 || m > 2048 || lda < m || (lda & 1) || ldx < m || (ldx & 1) || s < 1 || w < 1)
+    return SKB_ERR_ARG;
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  const int64_t N = n * (int64_t)s;
+  const int64_t C = std::max<int64_t>(4096, (N * (int64_t)w) / (16ll << 20) + 1);
+  const int64_t nch = (N + C - 1) / C;
+  int32_t* hist = (int32_t*)skb_ws_take(&ws, (size_t)nch * w * 4);
+  uint32_t* total = (uint32_t*)skb_ws_take(&ws, (size_t)w * 4);
+  uint64_t* start = (uint64_t*)skb_ws_take(&ws, (size_t)(w + 1) * 8);
+  int32_t* mem_j = (int32_t*)skb_ws_take(&ws, (size_t)std::max<int64_t>(N, 1) * 4);
+  double* mem_v = (double*)skb_ws_take(&ws, (size_t)std::max<int64_t>(N, 1) * 8);
+  unsigned int* counter = (unsigned int*)skb_ws_take(&ws, 16);
+  if (!hist || !total || !start || !mem_j || !mem_v || !counter) return SKB_ERR_WORKSPACE;
+  cudaMemsetAsync(hist, 0, (size_t)nch * w * 4, st);
+  cudaMemsetAsync(counter, 0, 16, st);
+  if (N > 0) {
+    bucket_hist_kernel<<<(unsigned)nch, 256, 0, st>>>(cols, N, C, w, hist);
+  }
+  bucket_chunk_prefix_kernel<<<(w + 255) / 256, 256, 0, st>>>(hist, (int)nch, w, total);
+  scan_buckets_kernel<<<1, 1024, 0, st>>>(total, start, w);
+  if (N > 0) {
+    const size_t csm = (size_t)w * 4;
+    if (csm > 48 * 1024) {
+      if (csm > 220 * 1024) return SKB_ERR_UNSUPPORTED;
+      cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)csm);
+    }
+    bucket_scatter_kernel<<<(unsigned)nch, 32, csm, st>>>(cols, vals, N, s, C, w, hist, start,
+                                                          mem_j, mem_v);
+  }
+  const size_t col_bytes = (size_t)lda * 8;
+  int stages = (int)std::min<size_t>(32, (200 * 1024) / col_bytes);
+  stages = std::max(stages, 2);
+  const size_t smem =
+      (((size_t)stages * (16 + sizeof(StageMeta)) + 127) & ~(size_t)127) + stages * col_bytes;
+  const int grid = std::min(skb_num_sms(), (int)std::max(1, w));
+  int rc = 0;
+  // one configured-smem watermark per kernel instantiation
+  static size_t conf[3] = {0, 0, 0};
+  auto launch = [&](auto kern, int which) {
+    if (smem > conf[which]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        rc = SKB_ERR_CUDA;
+      conf[which] = smem;
+    }
+    kern<<<grid, kConsumers + 32, smem, st>>>(A, lda, (int)m, d, start, mem_j, mem_v, w, stages,
+                                              counter, X, ldx);
+  };
+  if (m <= 512)
+    launch(sketch_accumulate_kernel<1>, 0);
+  else if (m <= 1024)
+    launch(sketch_accumulate_kernel<2>, 1);
+  else
+    launch(sketch_accumulate_kernel<4>, 2);
+  if (rc) return rc;
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_scale_columns(const double* A, int64_t m, int64_t n, int64_t lda,
+                                 const double* d, double* X, int64_t ldx, void* stream) {
+  if (n <= 0) return 0;
+  scale_columns_kernel<<<(unsigned)n, 128, 0, (cudaStream_t)stream>>>(A, lda, (int)m, n, d, X,
+                                                                      ldx);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_sketch_gather(const int32_t* cols, const double* vals, int32_t s, int64_t n,
+                                 const double* u, const double* x, const double* sv, double* v,
+                                 void* stream) {
+  if (n <= 0) return 0;
+  sketch_gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      cols, vals, s, n, u, x, sv, v);
+  return skb_launch_status(__func__);
+}

@@ -162,7 +162,8 @@ template <int R2, bool ZREG, class Op>
 __global__ void __launch_bounds__(256, 1)
     colstream_kernel(const double* __restrict__ A, int64_t lda, int m, int64_t n, int cb,
                      int stages, int64_t ngroups, const double* __restrict__ z,
-                     double* __restrict__ part, Op op) {
+                     double* __restrict__ part, Op op, const int* __restrict__ gate) {
+  if (gate && *gate) return;  // gated off (e.g. PCG already stopped)
   extern __shared__ __align__(128) unsigned char smem[];
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t col_bytes = (size_t)lda * 8, stage_bytes = (size_t)cb * col_bytes;
@@ -319,7 +320,9 @@ __global__ void __launch_bounds__(256, 1)
 
 // out[i] = sum_b part[b][i] (fixed order: 8 interleaved slices, combined in order) - sub[i]
 __global__ void reduce_partials_kernel(const double* __restrict__ part, int nb, int m,
-                                       const double* __restrict__ sub, double* __restrict__ out) {
+                                       const double* __restrict__ sub, double* __restrict__ out,
+                                       const int* __restrict__ gate) {
+  if (gate && *gate) return;
   __shared__ double sm[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int r = blockIdx.x * 32 + tx;
@@ -364,7 +367,8 @@ static StreamCfg stream_cfg(int m, int64_t n, int64_t lda) {
 
 template <int R2, bool ZREG, class Op>
 static int launch_r2(const StreamCfg& c, const double* A, int64_t lda, int m, int64_t n,
-                     const double* z, double* part, const Op& op, cudaStream_t st) {
+                     const double* z, double* part, const Op& op, cudaStream_t st,
+                     const int* gate) {
   auto kern = colstream_kernel<R2, ZREG, Op>;
   static size_t configured = 0;
   if (c.smem > configured) {
@@ -373,20 +377,26 @@ static int launch_r2(const StreamCfg& c, const double* A, int64_t lda, int m, in
       return SKB_ERR_CUDA;
     configured = c.smem;
   }
-  kern<<<c.grid, c.nw * 32, c.smem, st>>>(A, lda, m, n, c.cb, c.stages, c.ngroups, z, part, op);
+  kern<<<c.grid, c.nw * 32, c.smem, st>>>(A, lda, m, n, c.cb, c.stages, c.ngroups, z, part, op,
+                                          gate);
   return 0;
 }
 
+// Runs the streaming pass. With part_ext != nullptr the per-CTA partials are
+// written there (nparts_out receives their count) and the final reduction is
+// left to the caller (skb_reduce_partials); otherwise out = sum - sub.
 template <class Op>
 static int run_stream(const double* A, int64_t lda, int m, int64_t n, const double* z,
                       double* out, const double* sub, const Op& op, skb_ws* ws,
-                      cudaStream_t st) {
+                      cudaStream_t st, const int* gate = nullptr, double* part_ext = nullptr,
+                      int* nparts_out = nullptr) {
   if (m < 1 || n < 0 || lda < m || (lda & 1) || ((uintptr_t)A & 15)) return SKB_ERR_ARG;
   if (m > 2048) return SKB_ERR_UNSUPPORTED;
   if (n == 0) {
-    if (Op::kAxpy) {
+    if (nparts_out) *nparts_out = 0;
+    if (Op::kAxpy && !part_ext) {
       if (sub) {
-        reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(nullptr, 0, m, sub, out);
+        reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(nullptr, 0, m, sub, out, gate);
       } else {
         cudaMemsetAsync(out, 0, (size_t)m * 8, st);
       }
@@ -394,28 +404,29 @@ static int run_stream(const double* A, int64_t lda, int m, int64_t n, const doub
     return 0;
   }
   const StreamCfg c = stream_cfg(m, n, lda);
-  double* part = nullptr;
-  if (Op::kAxpy) {
+  double* part = part_ext;
+  if (Op::kAxpy && !part) {
     part = (double*)skb_ws_take(ws, (size_t)c.grid * m * 8);
     if (!part) return SKB_ERR_WORKSPACE;
   }
+  if (nparts_out) *nparts_out = c.grid;
   int rc;
   if (m <= 64)
-    rc = launch_r2<1, true>(c, A, lda, m, n, z, part, op, st);
+    rc = launch_r2<1, true>(c, A, lda, m, n, z, part, op, st, gate);
   else if (m <= 128)
-    rc = launch_r2<2, true>(c, A, lda, m, n, z, part, op, st);
+    rc = launch_r2<2, true>(c, A, lda, m, n, z, part, op, st, gate);
   else if (m <= 256)
-    rc = launch_r2<4, true>(c, A, lda, m, n, z, part, op, st);
+    rc = launch_r2<4, true>(c, A, lda, m, n, z, part, op, st, gate);
   else if (m <= 512)
-    rc = launch_r2<8, true>(c, A, lda, m, n, z, part, op, st);
+    rc = launch_r2<8, true>(c, A, lda, m, n, z, part, op, st, gate);
   else if (m <= 1024)
-    rc = launch_r2<16, true>(c, A, lda, m, n, z, part, op, st);
+    rc = launch_r2<16, true>(c, A, lda, m, n, z, part, op, st, gate);
   else
-    rc = launch_r2<32, false>(c, A, lda, m, n, z, part, op, st);
+    rc = launch_r2<32, false>(c, A, lda, m, n, z, part, op, st, gate);
   if (rc) return rc;
-  if (Op::kAxpy)
-    reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, c.grid, m, sub, out);
-  return cudaGetLastError() == cudaSuccess ? 0 : SKB_ERR_CUDA;
+  if (Op::kAxpy && !part_ext)
+    reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, c.grid, m, sub, out, gate);
+  return skb_launch_status(__func__);
 }
 
 }  // namespace skb
@@ -426,10 +437,21 @@ using namespace skb;
 
 extern "C" int skb_normal_apply(const double* A, int64_t m, int64_t n, int64_t lda,
                                 const double* d2, const double* z, double* u, const double* sub,
-                                void* workspace, size_t ws_bytes, void* stream) {
+                                const int* gate, void* workspace, size_t ws_bytes, void* stream) {
   SKB_WS;
   OpNormal op{d2};
-  return run_stream(A, lda, (int)m, n, z, u, sub, op, &ws, (cudaStream_t)stream);
+  return run_stream(A, lda, (int)m, n, z, u, sub, op, &ws, (cudaStream_t)stream, gate);
+}
+
+extern "C" int skb_normal_apply_partials(const double* A, int64_t m, int64_t n, int64_t lda,
+                                         const double* d2, const double* z, double* part,
+                                         int32_t* nparts_host, void* stream) {
+  OpNormal op{d2};
+  int np = 0;
+  int rc = run_stream(A, lda, (int)m, n, z, nullptr, nullptr, op, nullptr,
+                      (cudaStream_t)stream, nullptr, part, &np);
+  if (nparts_host) *nparts_host = np;
+  return rc;
 }
 
 extern "C" int skb_gemv(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,
@@ -487,8 +509,8 @@ extern "C" int skb_iterate(const double* A, int64_t m, int64_t n, int64_t lda, c
 extern "C" int skb_reduce_partials(const double* part, int32_t nparts, int64_t m,
                                    const double* sub, double* out, void* stream) {
   reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, (cudaStream_t)stream>>>(
-      part, nparts, (int)m, sub, out);
-  return cudaGetLastError() == cudaSuccess ? 0 : SKB_ERR_CUDA;
+      part, nparts, (int)m, sub, out, nullptr);
+  return skb_launch_status(__func__);
 }
 
 extern "C" size_t skb_stream_workspace_bytes(int64_t m) {

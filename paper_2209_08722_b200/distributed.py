@@ -1,0 +1,83 @@
+"""Column sharding across GPUs (one process per GPU, torch.distributed/NCCL).
+
+A is split into contiguous column blocks; rank g holds columns [j0, j1) and
+the matching slices of every n-vector (x, s, d, dx, ds, v, r_d). m-vectors
+(y, dy, p, r_p, PCG vectors) and the factor are replicated. The only data
+exchanges are the ones the math has:
+  - every A-pass that produces an m-vector: allreduce-sum of the local sum;
+  - the sketch ADW = sum_g A_g D_g W_g: allreduce-sum of the w x m partial;
+  - scalar reductions of n-vectors (sums, max, min).
+With world_size 1 every method is a no-op.
+"""
+
+from __future__ import annotations
+
+import torch
+
+try:
+    import torch.distributed as dist
+except Exception:  # pragma: no cover
+    dist = None
+
+SUM, MAX, MIN = "sum", "max", "min"
+
+
+class Comm:
+    def __init__(self, group=None):
+        self.group = group
+        if dist is not None and dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(group)
+            self.world = dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+
+    @property
+    def active(self) -> bool:
+        return self.world > 1
+
+    def shard(self, n: int):
+        """Balanced contiguous column range [j0, j1) of this rank."""
+        return shard_range(n, self.rank, self.world)
+
+    def allreduce_(self, t: torch.Tensor, op: str = SUM) -> torch.Tensor:
+        if self.world > 1:
+            rop = {SUM: dist.ReduceOp.SUM, MAX: dist.ReduceOp.MAX, MIN: dist.ReduceOp.MIN}[op]
+            dist.all_reduce(t, op=rop, group=self.group)
+        return t
+
+    def combine_(self, vals: torch.Tensor, ops) -> torch.Tensor:
+        """Combine a small vector of per-rank reduction results in place; ops[k]
+        says how entry k combines (sum / max / min)."""
+        if self.world == 1:
+            return vals
+        for kind in (SUM, MAX, MIN):
+            idx = [k for k, o in enumerate(ops) if o == kind]
+            if not idx:
+                continue
+            sel = torch.tensor(idx, device=vals.device)
+            part = vals.index_select(0, sel).clone()
+            self.allreduce_(part, kind)
+            vals.index_copy_(0, sel, part)
+        return vals
+
+    def gather_columns(self, t: torch.Tensor, n: int) -> torch.Tensor:
+        """All-gather the per-rank slices of an n-vector into the full vector."""
+        if self.world == 1:
+            return t
+        sizes = [shard_range(n, r, self.world) for r in range(self.world)]
+        width = max(j1 - j0 for j0, j1 in sizes)
+        buf = torch.zeros(width, dtype=t.dtype, device=t.device)
+        buf[: t.numel()].copy_(t)
+        out = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(out, buf, group=self.group)
+        return torch.cat([o[: j1 - j0] for o, (j0, j1) in zip(out, sizes)])
+
+    def barrier(self):
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+
+def shard_range(n: int, rank: int, world: int):
+    base, extra = divmod(n, world)
+    j0 = rank * base + min(rank, extra)
+    return j0, j0 + base + (1 if rank < extra else 0)

@@ -75,7 +75,7 @@ def _p(t):
 def normal_apply(A: DeviceMatrix, d2, z, out, sub=None):
     """out = A (d2 .* (A' z)) [- sub]   (krylov_solvers.py:46-47)."""
     ws, cap = _ws(A.m)
-    _lib.call("skb_normal_apply", A.cols, A.m, A.n, A.lda, d2, z, out, _p(sub), ws, cap,
+    _lib.call("skb_normal_apply", A.cols, A.m, A.n, A.lda, d2, z, out, _p(sub), None, ws, cap,
               stream_ptr())
     return out
 

@@ -1,0 +1,152 @@
+"""Sketch operators W and ADW on the device (reference sketching.py).
+
+build_sparse_embedding draws the bucket/sign hashes on the GPU, bit-exact with
+numpy's Philox stream (K1, csrc/skb_hash.cu); apply_sketch forms
+X = (A diag(d) W)' bucket-major, bit-exact with scipy's csr_matmat order
+(K2, csrc/skb_sketch.cu). Under column sharding every rank regenerates the
+whole hash stream (the Lemire compaction needs the global prefix), keeps its
+column slice, and the w x m partial sketches are allreduced.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import kernels as K
+from .errors import DimensionMismatch, InvalidDims, NonpositiveScaling
+from .runtime import F64, lda_for, require_cuda, stream_ptr, workspace
+
+
+def philox_key(seed: int):
+    """numpy Philox(seed) key = SeedSequence(seed).generate_state(2, uint64)."""
+    k = np.random.SeedSequence(int(seed)).generate_state(2, np.uint64)
+    return int(k[0]), int(k[1])
+
+
+@dataclass
+class SketchOperator:
+    """n x w sketch (reference SketchOperator, sketching.py:31-80).
+
+    For kind "sparse_sign", cols/vals are device tensors holding the s
+    buckets and values of this rank's rows [j0, j0 + n_local)."""
+
+    kind: str
+    n: int
+    w: int
+    s: int
+    seed: int
+    cols: torch.Tensor | None = None
+    vals: torch.Tensor | None = None
+    dense: torch.Tensor | None = None
+    j0: int = 0
+    words_used: int = 0
+
+    @property
+    def tag(self) -> tuple:
+        return (self.kind, self.n, self.w, self.s, self.seed)
+
+    def matvec(self, u: torch.Tensor) -> torch.Tensor:
+        """W u for a length-w device vector (local rows)."""
+        if u.shape != (self.w,):
+            raise DimensionMismatch(f"u has shape {tuple(u.shape)}, expected ({self.w},)")
+        if self.kind == "identity":
+            return u[self.j0:self.j0 + self.n_local].clone()
+        if self.kind != "sparse_sign":
+            raise NotImplementedError("Gaussian sketch matvec is not on the B200 path yet")
+        out = torch.empty(self.n_local, dtype=F64, device=u.device)
+        _lib.call("skb_sketch_gather", self.cols, self.vals, self.s, self.n_local, u, None, None,
+                  out, stream_ptr())
+        return out
+
+    @property
+    def n_local(self) -> int:
+        if self.cols is not None:
+            return int(self.cols.shape[0])
+        return self.n if self.kind != "identity" else self._n_local
+
+    _n_local: int = 0
+
+
+def auto_sketch_dims(m: int, n: int, delta: float):
+    """Reference auto_sketch_dims (sketching.py:83-90)."""
+    lg = max(1, math.ceil(math.log2(m / delta)))
+    w = min(n, 8 * m * lg)
+    return w, min(max(2, lg), w)
+
+
+def build_sparse_embedding(n: int, w: int, s: int, seed: int, rows=None,
+                           device=None) -> SketchOperator:
+    """Sparse sign embedding (sketching.py:93-119) drawn on the GPU.
+
+    rows = (j0, j1) keeps only this rank's rows (the full stream is drawn)."""
+    if not (1 <= s <= w):
+        raise InvalidDims(f"need 1 <= s <= w, got s={s}, w={w}")
+    if w > n * s:
+        raise InvalidDims(f"w={w} exceeds n*s={n * s}")
+    device = device or require_cuda()
+    k0, k1 = philox_key(seed)
+    cols, vals, used = K.sparse_embedding(k0, k1, n, w, s, device)
+    j0 = 0
+    if rows is not None and (rows[0] != 0 or rows[1] != n):
+        j0 = rows[0]
+        cols = cols[rows[0]:rows[1]].contiguous()
+        vals = vals[rows[0]:rows[1]].contiguous()
+    return SketchOperator(kind="sparse_sign", n=n, w=w, s=s, seed=int(seed), cols=cols, vals=vals,
+                          j0=j0, words_used=used)
+
+
+def build_identity_sketch(n: int, rows=None) -> SketchOperator:
+    """W = I for w >= n (sketching.py:122-128)."""
+    if n < 1:
+        raise InvalidDims(f"n must be positive, got {n}")
+    W = SketchOperator(kind="identity", n=n, w=n, s=0, seed=0)
+    W.j0 = rows[0] if rows else 0
+    W._n_local = (rows[1] - rows[0]) if rows else n
+    return W
+
+
+def build_gaussian_sketch(n: int, w: int, seed: int) -> SketchOperator:
+    """Dense Gaussian sketch (sketching.py:131-139): SURVEY.md §8(f) item 3,
+    not yet on the B200 path."""
+    if w < 1:
+        raise InvalidDims(f"w must be positive, got {w}")
+    raise NotImplementedError("the Gaussian sketch (K9) is not implemented on the B200 path yet")
+
+
+def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = True):
+    """X = (A diag(d) W)' as a DeviceMatrix with w 'columns' of length m
+    (sketching.py:142-161). lp: DeviceLP (this rank's columns)."""
+    A = lp.A
+    if d.shape != (A.n,):
+        raise DimensionMismatch(f"d has shape {tuple(d.shape)}, expected ({A.n},)")
+    if W.n != lp.n:
+        raise DimensionMismatch(f"sketch has {W.n} rows, expected {lp.n}")
+    if check_positive and lp.vec_stats(d)[3] <= 0.0:
+        raise NonpositiveScaling("column scaling d must be strictly positive")
+    m = A.m
+    ldx = lda_for(m)
+    X = torch.empty((W.w, ldx), dtype=F64, device=d.device)
+    if W.kind == "identity":
+        if lp.comm.active:
+            X.zero_()
+            sub = X[lp.j0:lp.j0 + A.n]
+            _lib.call("skb_scale_columns", A.cols, m, A.n, A.lda, d, sub, ldx, stream_ptr())
+        else:
+            _lib.call("skb_scale_columns", A.cols, m, A.n, A.lda, d, X, ldx, stream_ptr())
+    elif W.kind == "sparse_sign":
+        need = int(_lib.lib().skb_sketch_workspace_bytes(A.n, W.w, W.s))
+        ws, cap = workspace(need)
+        _lib.call("skb_sketch_apply", A.cols, m, A.n, A.lda, d, W.cols, W.vals, W.s, W.w, X, ldx,
+                  ws, cap, stream_ptr())
+    else:
+        raise NotImplementedError("Gaussian sketch apply (K9) is not implemented yet")
+    if ldx != m:
+        X[:, m:].zero_()
+    if lp.comm.active:
+        lp.comm.allreduce_(X)
+    return K.DeviceMatrix(X, m)

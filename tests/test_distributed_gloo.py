@@ -1,0 +1,67 @@
+"""Column-sharded host logic on world_size 2 over gloo (CPU): shard ranges,
+the allreduce of per-rank m-vector partials, scalar combines (sum / max /
+min) and the column gather used by the solve report."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2209_08722_b200.distributed import Comm
+        comm = Comm()
+        assert (comm.rank, comm.world) == (rank, world)
+        m, n = 7, 1003
+        g = np.random.default_rng(0)
+        A = g.standard_normal((m, n))
+        x = g.standard_normal(n)
+        j0, j1 = comm.shard(n)
+        # per-rank column-block partial of A x (what the streaming kernel returns)
+        part = torch.from_numpy(A[:, j0:j1] @ x[j0:j1])
+        comm.allreduce_(part)
+        full = A @ x
+        err = float(np.max(np.abs(part.numpy() - full)) / np.max(np.abs(full)))
+        # scalar stats combine: sum, max, min in one call
+        loc = x[j0:j1]
+        st = torch.tensor([float((loc * loc).sum()), float(loc.max()), float(loc.min())],
+                          dtype=torch.float64)
+        comm.combine_(st, ("sum", "max", "min"))
+        ok_stats = (abs(st[0].item() - float(x @ x)) <= 1e-12 * float(x @ x)
+                    and st[1].item() == x.max() and st[2].item() == x.min())
+        gathered = comm.gather_columns(torch.from_numpy(x[j0:j1].copy()), n).numpy()
+        q.put((rank, err, ok_stats, bool(np.array_equal(gathered, x)), (j0, j1)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_host_logic_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    assert res[0][4] == (0, 502) and res[1][4] == (502, 1003)
+    for _, err, ok_stats, ok_gather, _ in res:
+        assert err <= 1e-13 and ok_stats and ok_gather

@@ -1,0 +1,334 @@
+"""GPU parity of the sketch -> factor -> PCG -> step path against the oracle
+and the reference's golden traces (SURVEY.md §8(c) protocol)."""
+
+import copy
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import GOLDEN
+from oracle import chash
+from oracle import ipm_oracle as O
+from paper_2209_08722_b200.problems import wide_dense_lp
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2209_08722_b200 as P
+    return P
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def _h(t):
+    return t.detach().cpu().numpy()
+
+
+def _dlp(P, A, b=None, c=None):
+    from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
+    m, n = A.shape
+    b = np.zeros(m) if b is None else b
+    c = np.ones(n) if c is None else c
+    return DeviceLP.from_host(LinearProgram(A, b, c))
+
+
+# ------------------------------------------------------------------ sketch
+
+
+def test_sketch_apply_golden_bits(P):
+    from paper_2209_08722_b200 import sketching as S
+    g = np.load(os.path.join(GOLDEN, "adw_small.npz"))
+    A, d = g["A"], g["d"]
+    lp = _dlp(P, A)
+    for s in (1, 4):
+        W = S.build_sparse_embedding(A.shape[1], 64, s, int(g[f"seed_s{s}"]))
+        X = S.apply_sketch(lp, _t(d), W)
+        adw = _h(X.cols)[:, :A.shape[0]].T
+        assert np.array_equal(adw, g[f"adw_s{s}"]), s
+
+
+@pytest.mark.parametrize("m,n,w,s", [(100, 10_000, 400, 1), (100, 10_000, 400, 4),
+                                     (37, 5000, 300, 2), (1000, 20_000, 4000, 1),
+                                     (700, 8000, 2000, 3)])
+def test_sketch_apply_bit_exact_vs_c_oracle(P, m, n, w, s):
+    from paper_2209_08722_b200 import sketching as S
+    g = np.random.Generator(np.random.Philox(m + n))
+    A = g.standard_normal((m, n))
+    d = 10.0 ** g.uniform(-3, 3, n)
+    lp = _dlp(P, A)
+    seed = 1234 + s
+    W = S.build_sparse_embedding(n, w, s, seed)
+    X = S.apply_sketch(lp, _t(d), W)
+    cols, vals = O.sparse_embedding(n, w, s, seed)
+    ref = chash.adw_dense(A, d, cols, vals, w)
+    assert np.array_equal(_h(X.cols)[:, :m].T, ref)
+
+
+def test_identity_sketch(P):
+    from paper_2209_08722_b200 import sketching as S
+    g = np.random.Generator(np.random.Philox(5))
+    A = g.standard_normal((6, 40))
+    d = g.random(40) + 0.1
+    lp = _dlp(P, A)
+    X = S.apply_sketch(lp, _t(d), S.build_identity_sketch(40))
+    assert np.array_equal(_h(X.cols)[:, :6].T, A * d[None, :])
+
+
+# ------------------------------------------------------------------ factor
+
+
+def _factor_case(P, m, n, w, s, span=2.0, seed=0):
+    from paper_2209_08722_b200 import preconditioning as PC
+    from paper_2209_08722_b200 import sketching as S
+    g = np.random.Generator(np.random.Philox(seed))
+    A = g.standard_normal((m, n))
+    d = 10.0 ** g.uniform(-span, span / 2, n)
+    lp = _dlp(P, A)
+    W = S.build_sparse_embedding(n, w, s, seed + 7)
+    X = S.apply_sketch(lp, _t(d), W)
+    f = PC.build_preconditioner(X, sketch_tag=W.tag)
+    cols, vals = O.sparse_embedding(n, w, s, seed + 7)
+    Wo = O.Sketch("sparse_sign", n, w, s, seed + 7, cols=cols, vals=vals)
+    fo = O.Factor(O.apply_sketch(sp.csr_matrix(A), d, Wo))
+    return g, A, d, lp, W, f, Wo, fo
+
+
+@pytest.mark.parametrize("m,n,w,s,span", [(20, 2000, 80, 4, 2.0), (100, 10_000, 400, 1, 3.0),
+                                          (300, 6000, 1200, 4, 4.0), (1000, 12_000, 4000, 1, 2.0),
+                                          (65, 3000, 260, 2, 6.0)])
+def test_factor_inverse_and_pinv(P, m, n, w, s, span):
+    from paper_2209_08722_b200 import preconditioning as PC
+    g, A, d, lp, W, f, Wo, fo = _factor_case(P, m, n, w, s, span)
+    r = g.standard_normal(m)
+    z = _h(PC.apply_inv(f, _t(r)))
+    z_ref = fo.inv(r)
+    assert np.max(np.abs(z - z_ref)) <= 1e-9 * np.max(np.abs(z_ref))
+    u = _h(PC.apply_pinv_adw(f, _t(r)))
+    u_ref = fo.pinv(r)
+    assert np.max(np.abs(u - u_ref)) <= 1e-9 * np.max(np.abs(u_ref))
+    # r'Q^-1 r is what the PCG trace records
+    assert abs(r @ z - r @ z_ref) <= 1e-12 * abs(r @ z_ref)
+
+
+def test_rank_deficient_width(P):
+    from paper_2209_08722_b200 import preconditioning as PC
+    from paper_2209_08722_b200.kernels import DeviceMatrix
+    X = DeviceMatrix.from_host(np.random.default_rng(0).standard_normal((10, 4)))  # w=4 < m=10
+    with pytest.raises(P.RankDeficient):
+        PC.build_preconditioner(X)
+
+
+def test_rank_deficient_collapse(P):
+    from paper_2209_08722_b200 import preconditioning as PC
+    from paper_2209_08722_b200.kernels import DeviceMatrix
+    M = np.random.default_rng(1).standard_normal((8, 50))
+    M[3] = M[2]  # two equal rows of ADW: exactly rank deficient
+    with pytest.raises(P.RankDeficient):
+        PC.build_preconditioner(DeviceMatrix.from_host(M))
+
+
+# --------------------------------------------------------------------- PCG
+
+
+@pytest.mark.parametrize("m,n,w,s,span,t", [(20, 2000, 80, 4, 2.0, 30), (100, 10_000, 400, 1, 3.0, 19),
+                                            (300, 6000, 1200, 4, 4.0, 25)])
+def test_pcg_matches_oracle(P, m, n, w, s, span, t):
+    from paper_2209_08722_b200 import krylov_solvers as KS
+    g, A, d, lp, W, f, Wo, fo = _factor_case(P, m, n, w, s, span, seed=3)
+    p = g.standard_normal(m)
+    op = KS.NormalOperator(lp, _t(d))
+    dy, tr = KS.pcg(op, f, _t(p), t, 1e-5)
+    dyo, norms, its, conv = O.pcg(O.NormalOp(sp.csr_matrix(A), d), fo, p, t, 1e-5)
+    assert tr.iterations == its and tr.converged == conv
+    f0 = norms[0]
+    assert np.max(np.abs(np.array(tr.residual_norms) - np.array(norms))) <= 1e-9 * f0
+    assert np.max(np.abs(_h(dy) - dyo)) <= 1e-8 * np.max(np.abs(dyo))
+
+
+def test_pcg_zero_rhs_and_breakdown(P):
+    from paper_2209_08722_b200 import krylov_solvers as KS
+    g, A, d, lp, W, f, Wo, fo = _factor_case(P, 20, 2000, 80, 4, 2.0, seed=4)
+    op = KS.NormalOperator(lp, _t(d))
+    dy, tr = KS.pcg(op, f, _t(np.zeros(20)), 10, 1e-8)
+    assert tr.converged and tr.iterations == 0 and not _h(dy).any()
+
+    class NegativeOp:
+        m = 20
+
+        def apply(self, v):
+            return -v
+
+    with pytest.raises(P.Breakdown):
+        KS.pcg(NegativeOp(), f, _t(np.ones(20)), 5, 1e-6)
+
+
+# ---------------------------------------------------------- IPM trajectories
+
+
+def _device_solve(P, lpd, **kw):
+    from paper_2209_08722_b200 import ipm_core as IC
+    from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
+    dlp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c, lpd.name))
+    start = kw.pop("start", None)
+    if start is None:
+        start = IC.make_iterate(dlp, lpd.x0, lpd.y0, lpd.s0)
+    else:
+        start = IC.make_iterate(dlp, *start)
+    return IC.solve(dlp, start, IC.IpmParams(**kw))
+
+
+def _reordered_oracle(monkeypatch, lpd, **prm):
+    """The reference algorithm with one legitimate change: the normal-operator
+    matvec summed in dense-BLAS order instead of scipy CSR order. Its distance
+    from the golden trace is the reference's own rounding floor; late IPM steps
+    amplify it (v is a cancellation residual), so per-step tolerances are
+    max(1e-9, 4 x that floor) -- see DESIGN.md 'Parity'."""
+    Ad = np.ascontiguousarray(lpd.A)
+    monkeypatch.setattr(O.NormalOp, "apply", lambda self, v: Ad @ (self.d2 * (Ad.T @ v)))
+    A = sp.csr_matrix(lpd.A)
+    start = prm.pop("start", None)
+    if start is None:
+        st = O.make_iterate(A, lpd.b, lpd.c, lpd.x0, lpd.y0, lpd.s0)
+    else:
+        st = O.make_iterate(A, lpd.b, lpd.c, *start)
+    rep = O.solve(A, lpd.b, lpd.c, st, O.Params(**prm))
+    monkeypatch.undo()
+    return rep
+
+
+def _floors(ref, gold):
+    """Cumulative per-step deviation of the reordered reference from gold."""
+    mu = np.abs(np.array(ref["mu_trace"]) - np.array(gold["mu_trace"])) / np.array(gold["mu_trace"])
+    rn = [0.0] + [np.max(np.abs(np.array(a["inner_residual_norms"]) -
+                                np.array(b["inner_residual_norms"]))) / b["f_norm0"]
+                  for a, b in zip(ref["steps"], gold["steps"])]
+    return np.maximum.accumulate(mu), np.maximum.accumulate(np.array(rn))
+
+
+def _check_trace(rep, gold, ref=None, obj_rtol=1e-8):
+    assert rep.outer == gold["outer"]
+    assert [r.inner_iterations for r in rep.steps] == gold["inner_iterations"]
+    assert [r.sketch_seed for r in rep.steps] == [s["sketch_seed"] for s in gold["steps"]]
+    assert [r.v_retries for r in rep.steps] == [s["v_retries"] for s in gold["steps"]]
+    if ref is not None:
+        fmu, frn = _floors(ref, gold)
+    else:
+        fmu = frn = np.zeros(rep.outer + 1)
+    mu_dev = np.abs(np.array(rep.mu_trace) - np.array(gold["mu_trace"])) / np.array(gold["mu_trace"])
+    assert np.all(mu_dev <= np.maximum(1e-9, 4 * fmu)), (mu_dev, fmu)
+    for k, (r, gs) in enumerate(zip(rep.steps, gold["steps"])):
+        dev = np.max(np.abs(np.array(r.inner_residual_norms) -
+                            np.array(gs["inner_residual_norms"]))) / gs["f_norm0"]
+        assert dev <= max(1e-9, 4 * frn[k + 1]), (k, dev, frn[k + 1])
+    assert abs(rep.objective - gold["objective"]) <= obj_rtol * abs(gold["objective"])
+
+
+def test_small_lp_trajectories_both_modes(P, monkeypatch):
+    with open(os.path.join(GOLDEN, "small_traces.json")) as f:
+        gold = json.load(f)
+    lpd = wide_dense_lp(40, 3000, 5)
+    kw = dict(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5, w=160, s=4, tol_outer=1e-7,
+              seed=3)
+    rep = _device_solve(P, lpd, **kw)
+    _check_trace(rep, gold["feasible"], _reordered_oracle(monkeypatch, lpd, **kw))
+    start = (np.ones(3000), np.zeros(40), np.ones(3000))
+    kw = dict(mode="infeasible", gamma=0.5, sigma=0.5, w=160, s=4, tol_outer=1e-7, seed=4,
+              max_outer=60)
+    rep = _device_solve(P, lpd, start=start, **kw)
+    _check_trace(rep, gold["infeasible"], _reordered_oracle(monkeypatch, lpd, start=start, **kw))
+
+
+def test_config1_trajectory_s4(P, monkeypatch):
+    with open(os.path.join(GOLDEN, "c1_traces.json")) as f:
+        gold = json.load(f)
+    lpd = wide_dense_lp(100, 10_000, 0)
+    kw = dict(mode="feasible", gamma=gold["gamma_run"], sigma=0.5, w=400, s=4, tol_outer=1e-6,
+              seed=0)
+    rep = _device_solve(P, lpd, **kw)
+    _check_trace(rep, gold["s4"], _reordered_oracle(monkeypatch, lpd, **kw))
+
+
+def test_config1_lockstep_s1(P):
+    """s=1 CountSketch is rounding-chaotic over whole trajectories (SURVEY.md
+    App. B.3), so parity is per step: from the device iterate and the same
+    outer-RNG state, the oracle step must agree with the device step."""
+    from paper_2209_08722_b200 import ipm_core as IC
+    from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
+    lpd = wide_dense_lp(100, 10_000, 0)
+    Acsr = sp.csr_matrix(lpd.A)
+    dlp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c))
+    gamma = lpd.gamma_run(0.1)
+    prm = IC.IpmParams(mode="feasible", gamma=gamma, sigma=0.5, w=400, s=1, tol_outer=1e-6)
+    oprm = O.Params(mode="feasible", gamma=gamma, sigma=0.5, w=400, s=1, tol_outer=1e-6)
+    it = IC.make_iterate(dlp, lpd.x0, lpd.y0, lpd.s0)
+    rng = np.random.Generator(np.random.Philox(0))
+    mu0, r0 = it.mu, max(it.residual_norm, 1e-300)
+    Ad = np.ascontiguousarray(lpd.A)
+    csr_apply = O.NormalOp.apply
+
+    factor_init = O.Factor.__init__
+
+    def perturbed_init(self, ADW, tag=None):  # sigma(ADW) * (1 + 1e-15 xi): SVD-level noise
+        factor_init(self, ADW, tag)
+        xi = np.random.default_rng(self.sig.size).standard_normal(self.sig.size)
+        self.sig = self.sig * (1.0 + 1e-15 * xi)
+
+    def oracle_step(state, ox, oy, os_, k, variant):
+        if variant == "dense":
+            O.NormalOp.apply = lambda self, v: Ad @ (self.d2 * (Ad.T @ v))
+        elif variant == "sigma":
+            O.Factor.__init__ = perturbed_init
+        try:
+            orng = np.random.Generator(np.random.Philox(0))
+            orng.bit_generator.state = copy.deepcopy(state)
+            oit = O.make_iterate(Acsr, lpd.b, lpd.c, ox, oy, os_, k)
+            return O.ipm_step(Acsr, lpd.b, lpd.c, oit, oprm, orng, r0, mu0)[1]
+        finally:
+            O.NormalOp.apply = csr_apply
+            O.Factor.__init__ = factor_init
+
+    def dev(a, b, key):
+        return abs(a[key] - b[key]) / abs(b[key])
+
+    strict_steps = 0
+    for k in range(40):
+        if it.mu <= 1e-6 * max(1.0, mu0):
+            break
+        state = copy.deepcopy(rng.bit_generator.state)
+        ox, oy, os_ = _h(it.x), _h(it.y), _h(it.s)
+        new, rec = IC.ipm_step(dlp, it, prm, rng, r0, mu0)
+        r = rec.to_dict()
+        o1 = oracle_step(state, ox, oy, os_, k, "csr")
+        alts = [oracle_step(state, ox, oy, os_, k, v) for v in ("dense", "sigma")]
+        assert r["sketch_seed"] == o1["sketch_seed"]
+        keys = ("inner_iterations", "v_retries", "rank_retries")
+        same = all(o1[q] == o[q] for o in alts for q in keys)
+        if same:  # non-chaotic step: counts exact, values within the reference's floor
+            strict_steps += 1
+            for q in keys:
+                assert r[q] == o1[q], (k, q)
+            for q in ("mu_after", "alpha_bar", "alpha_tilde"):
+                floor = max(dev(o, o1, q) for o in alts)
+                assert dev(r, o1, q) <= max(1e-9, 4 * floor), (k, q, dev(r, o1, q), floor)
+            n1 = len(o1["inner_residual_norms"])
+            fl = max(np.max(np.abs(np.array(o["inner_residual_norms"][:n1]) -
+                                   np.array(o1["inner_residual_norms"]))) / o1["f_norm0"]
+                     for o in alts)
+            dv = np.max(np.abs(np.array(r["inner_residual_norms"]) -
+                               np.array(o1["inner_residual_norms"]))) / o1["f_norm0"]
+            assert dv <= max(1e-9, 4 * fl), (k, dv, fl)
+        else:  # the reference itself is chaotic here: match one of its variants
+            assert any(r["inner_iterations"] == o["inner_iterations"] for o in [o1] + alts), k
+        it = new
+    assert strict_steps >= 10
