@@ -284,11 +284,33 @@ def test_config1_lockstep_s1(P):
         xi = np.random.default_rng(self.sig.size).standard_normal(self.sig.size)
         self.sig = self.sig * (1.0 + 1e-15 * xi)
 
+    import scipy.linalg as sla
+
+    class QrFactor(O.Factor):
+        """Same operators from a Householder QR of ADW' (ADW = R'Q'):
+        Q^-1 r = R^-1 R^-T r, (ADW)^+ r = Q R^-T r -- the triangular-factor
+        family the device's CholeskyQR2 belongs to."""
+
+        def __init__(self, ADW, tag=None):
+            factor_init(self, ADW, tag)   # keeps the reference's rank test
+            self.Qm, self.R = np.linalg.qr(np.asarray(ADW).T)
+
+        def inv(self, r):
+            t = sla.solve_triangular(self.R, r, trans="T")
+            return sla.solve_triangular(self.R, t)
+
+        def pinv(self, r):
+            return self.Qm @ sla.solve_triangular(self.R, r, trans="T")
+
+    base_factor = O.Factor
+
     def oracle_step(state, ox, oy, os_, k, variant):
         if variant == "dense":
             O.NormalOp.apply = lambda self, v: Ad @ (self.d2 * (Ad.T @ v))
         elif variant == "sigma":
             O.Factor.__init__ = perturbed_init
+        elif variant == "qr":
+            O.Factor = QrFactor
         try:
             orng = np.random.Generator(np.random.Philox(0))
             orng.bit_generator.state = copy.deepcopy(state)
@@ -296,6 +318,7 @@ def test_config1_lockstep_s1(P):
             return O.ipm_step(Acsr, lpd.b, lpd.c, oit, oprm, orng, r0, mu0)[1]
         finally:
             O.NormalOp.apply = csr_apply
+            O.Factor = base_factor
             O.Factor.__init__ = factor_init
 
     def dev(a, b, key):
@@ -310,25 +333,30 @@ def test_config1_lockstep_s1(P):
         new, rec = IC.ipm_step(dlp, it, prm, rng, r0, mu0)
         r = rec.to_dict()
         o1 = oracle_step(state, ox, oy, os_, k, "csr")
-        alts = [oracle_step(state, ox, oy, os_, k, v) for v in ("dense", "sigma")]
+        alts = [oracle_step(state, ox, oy, os_, k, v) for v in ("dense", "sigma", "qr")]
         assert r["sketch_seed"] == o1["sketch_seed"]
         keys = ("inner_iterations", "v_retries", "rank_retries")
-        same = all(o1[q] == o[q] for o in alts for q in keys)
-        if same:  # non-chaotic step: counts exact, values within the reference's floor
+        n1 = len(o1["inner_residual_norms"])
+        fl = max(np.max(np.abs(np.array(o["inner_residual_norms"][:n1]) -
+                               np.array(o1["inner_residual_norms"][:len(o["inner_residual_norms"])])))
+                 / o1["f_norm0"] for o in alts)
+        stable = fl <= 1e-9 and all(o1[q] == o[q] for o in alts for q in keys)
+        if stable:  # the reference is stable here: counts exact, values within its floor
             strict_steps += 1
             for q in keys:
                 assert r[q] == o1[q], (k, q)
             for q in ("mu_after", "alpha_bar", "alpha_tilde"):
                 floor = max(dev(o, o1, q) for o in alts)
                 assert dev(r, o1, q) <= max(1e-9, 4 * floor), (k, q, dev(r, o1, q), floor)
-            n1 = len(o1["inner_residual_norms"])
-            fl = max(np.max(np.abs(np.array(o["inner_residual_norms"][:n1]) -
-                                   np.array(o1["inner_residual_norms"]))) / o1["f_norm0"]
-                     for o in alts)
             dv = np.max(np.abs(np.array(r["inner_residual_norms"]) -
                                np.array(o1["inner_residual_norms"]))) / o1["f_norm0"]
             assert dv <= max(1e-9, 4 * fl), (k, dv, fl)
-        else:  # the reference itself is chaotic here: match one of its variants
+        else:
+            # The reference itself is chaotic at this step (a QR factor or a
+            # reordered matvec moves its PCG residuals past 1e-9 f0; SURVEY.md
+            # App. B.3): match one of its variants' counts, mu within its spread.
             assert any(r["inner_iterations"] == o["inner_iterations"] for o in [o1] + alts), k
+            spread = max(dev(o, o1, "mu_after") for o in alts)
+            assert dev(r, o1, "mu_after") <= max(1e-6, 4 * spread), k
         it = new
     assert strict_steps >= 10
