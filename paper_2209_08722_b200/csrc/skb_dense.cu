@@ -190,53 +190,105 @@ __global__ void gemm_splitk_reduce_kernel(GemmArgs g, int nbatch) {
 // ----------------------------------------------------------------- Cholesky
 constexpr int NB = 64;
 
-// Unblocked Cholesky of the nb x nb diagonal block at (k0, k0) (lower, in place).
-__global__ void __launch_bounds__(256) potrf_diag_kernel(double* G, int64_t ld, int k0, int nb,
-                                                          int* status) {
-  __shared__ double a[NB][NB + 1];
+// Unblocked right-looking Cholesky of the 64 x 64 diagonal block at (k0, k0),
+// lower, in place, plus its inverse Dinv = L11^-1 (64 x 64, row-major) which
+// turns the panel TRSM into a GEMM and seeds the triangular inverse.
+// Thread i keeps row i in registers, ROTATED so the current column is always
+// r[0] (static register indices with a runtime step loop: a fully unrolled
+// version thrashed the I-cache, a shared-memory version serialised on
+// load/store aliasing — both >100 us per block). Column c of L is broadcast
+// through shared memory; the <= 63 updates of a step are independent FMAs.
+constexpr int kRot = 8;  // steps per register rotation
+
+__global__ void __launch_bounds__(NB) potrf_diag_kernel(double* G, int64_t ld, int k0, int nb,
+                                                         int* status, double* Dinv) {
+  // col[] is padded so the unpredicated updates may read past row 63: entries
+  // that land in a row's upper triangle are never used as factor values.
+  __shared__ double col[2 * NB + kRot];
+  __shared__ double lt[NB][NB + 1];  // lt[q][r] = L[r][q]
+  __shared__ double rl_s[kRot];
   __shared__ int bad;
-  const int tid = threadIdx.x;
-  for (int t = tid; t < nb * nb; t += blockDim.x) {
-    const int i = t / nb, j = t % nb;
-    a[i][j] = G[(int64_t)(k0 + i) * ld + k0 + j];
-  }
-  if (tid == 0) bad = 0;
+  const int i = threadIdx.x;
+  double* grow = G + (int64_t)(k0 + i) * ld + k0;
+  double r[NB + kRot];  // r[k] = A[i][c0 + k] for the current rotation base c0
+#pragma unroll
+  for (int k = 0; k < NB; ++k) r[k] = k <= i ? grow[k] : 0.0;
+#pragma unroll
+  for (int k = NB; k < NB + kRot; ++k) r[k] = 0.0;
+  for (int k = i; k < 2 * NB + kRot; k += NB) col[k] = 0.0;
+  if (i == 0) bad = 0;
   __syncthreads();
-  for (int c = 0; c < nb; ++c) {
-    if (tid == 0) {
-      const double piv = a[c][c];
-      if (!(piv > 0.0)) bad = 1;
-      a[c][c] = sqrt(piv);
+  for (int c0 = 0; c0 < NB; c0 += kRot) {
+#pragma unroll
+    for (int u = 0; u < kRot; ++u) {
+      const int c = c0 + u;
+      if (i == c) {
+        const double piv = r[u];
+        if (!(piv > 0.0)) bad = 1;
+        const double l = sqrt(piv);
+        col[c] = l;
+        rl_s[u] = 1.0 / l;
+      }
+      __syncthreads();
+      if (bad) break;
+      double lic = 0.0;
+      if (i > c) {
+        lic = r[u] * rl_s[u];
+        col[i] = lic;
+      }
+      __syncthreads();
+      if (i >= c) {
+        const double v = i == c ? col[c] : lic;
+        grow[c] = v;
+        lt[c][i] = v;
+      }
+#pragma unroll
+      for (int k = u + 1; k < NB + u; ++k) r[k] -= lic * col[c0 + k];  // lic == 0 for i <= c
+      __syncthreads();
     }
-    __syncthreads();
     if (bad) break;
-    const double l = a[c][c];
-    for (int i = c + 1 + tid; i < nb; i += blockDim.x) a[i][c] = a[i][c] / l;
-    __syncthreads();
-    const int rem = nb - c - 1;
-    for (int t = tid; t < rem * rem; t += blockDim.x) {
-      const int i = c + 1 + t / rem, j = c + 1 + t % rem;
-      if (j <= i) a[i][j] -= a[i][c] * a[j][c];
-    }
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NB; ++k) r[k] = r[k + kRot];
   }
   if (bad) {
-    if (tid == 0) atomicOr(status, ST_CHOL_FAIL);
+    if (i == 0) atomicOr(status, ST_CHOL_FAIL);
     return;
   }
-  for (int t = tid; t < nb * nb; t += blockDim.x) {
-    const int i = t / nb, j = t % nb;
-    G[(int64_t)(k0 + i) * ld + k0 + j] = j <= i ? a[i][j] : 0.0;
+  for (int k = i + 1; k < NB; ++k) grow[k] = 0.0;
+  if (!Dinv) return;
+  // Column i of L11^-1 by right-looking forward substitution, rotated the same
+  // way: x[u] is entry q = q0 + u; x_q /= L_qq, then x_{q+k} -= L_{q+k,q} x_q.
+  double x[NB + kRot];
+#pragma unroll
+  for (int k = 0; k < NB + kRot; ++k) x[k] = 0.0;
+  x[0] = 1.0;
+  const int q_start = i & ~(kRot - 1);  // entries above i stay zero
+#pragma unroll
+  for (int k = 0; k < NB; ++k) x[k] = (k == i - q_start) ? 1.0 : 0.0;
+  for (int q = 0; q < q_start; ++q) Dinv[(int64_t)q * NB + i] = 0.0;
+  for (int q0 = q_start; q0 < NB; q0 += kRot) {
+#pragma unroll
+    for (int u = 0; u < kRot; ++u) {
+      const int q = q0 + u;
+      const double x0 = q < i ? 0.0 : x[u] / lt[q][q];
+      Dinv[(int64_t)q * NB + i] = x0;
+#pragma unroll
+      for (int k = u + 1; k < NB + u; ++k)
+        if (q0 + k < NB) x[k] -= lt[q][q0 + k] * x0;
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) x[k] = x[k + kRot];
   }
 }
 
-// Panel: rows i in [k0+nb, M) of columns [k0, k0+nb): x L11' = a.
+// Panel: rows i in [k0+nb, M) of columns [k0, k0+nb): solve x L11' = a by
+// right-looking substitution (the updates of one step are independent).
 __global__ void __launch_bounds__(128) trsm_panel_kernel(double* G, int64_t ld, int k0, int nb,
                                                           int M) {
   __shared__ double l[NB][NB + 1];
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
-    const int i = t / nb, j = t % nb;
-    l[i][j] = G[(int64_t)(k0 + i) * ld + k0 + j];
+  for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
+    const int a = t / NB, b = t % NB;
+    l[b][a] = G[(int64_t)(k0 + a) * ld + k0 + b];  // transposed: l[c][q] = L11[q][c]
   }
   __syncthreads();
   const int i = k0 + nb + blockIdx.x * blockDim.x + threadIdx.x;
@@ -244,19 +296,15 @@ __global__ void __launch_bounds__(128) trsm_panel_kernel(double* G, int64_t ld, 
   double* row = G + (int64_t)i * ld + k0;
   double x[NB];
 #pragma unroll
-  for (int c = 0; c < NB; ++c) x[c] = c < nb ? row[c] : 0.0;
+  for (int c = 0; c < NB; ++c) x[c] = row[c];
 #pragma unroll
   for (int c = 0; c < NB; ++c) {
-    if (c < nb) {
-      double t = x[c];
+    x[c] = x[c] / l[c][c];
 #pragma unroll
-      for (int q = 0; q < c; ++q) t -= x[q] * l[c][q];
-      x[c] = t / l[c][c];
-    }
+    for (int q = c + 1; q < NB; ++q) x[q] -= x[c] * l[c][q];
   }
 #pragma unroll
-  for (int c = 0; c < NB; ++c)
-    if (c < nb) row[c] = x[c];
+  for (int c = 0; c < NB; ++c) row[c] = x[c];
 }
 
 // Inverse of each 64x64 lower-triangular diagonal block: Linv[b] = L[b]^-1.
@@ -351,6 +399,39 @@ __global__ void diag_stats_kernel(const double* G, int64_t ld, int m, double* ou
       out[1] = mn;
       out[2] = mx;
     }
+  }
+}
+
+// dprod[i] = |L_ii| (init) or dprod[i] * |L_ii|: diag of a product of triangular factors.
+__global__ void diag_accum_kernel(const double* L, int64_t ld, int m, double* dprod, int init) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double v = fabs(L[(int64_t)i * ld + i]);
+  dprod[i] = init ? v : dprod[i] * v;
+}
+
+// out[1] = min v, out[2] = max v (single CTA).
+__global__ void vec_minmax_kernel(const double* v, int m, double* out) {
+  __shared__ double smn[32], smx[32];
+  double mn = INFINITY, mx = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    mn = fmin(mn, v[i]);
+    mx = fmax(mx, v[i]);
+  }
+  mn = warp_min(mn);
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) {
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mn = fmin(mn, smn[w]);
+      mx = fmax(mx, smx[w]);
+    }
+    out[1] = mn;
+    out[2] = mx;
   }
 }
 
@@ -469,18 +550,27 @@ static int round_pad(int m) {
 extern "C" int32_t skb_factor_padded_dim(int32_t m) { return round_pad(m); }
 
 // Blocked right-looking Cholesky of the (Mp x Mp, ld) lower part in place.
+// Per 64-wide panel: diagonal factor + its inverse (one CTA), panel
+// L21 = A21 L11^-T as a DMMA GEMM (in place: each CTA owns whole rows),
+// trailing update A22 -= L21 L21' on the lower tiles.
 static int potrf(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStream_t st) {
+  const size_t mark = ws->off;
+  double* Dinv = (double*)skb_ws_take(ws, (size_t)NB * NB * 8);
+  if (!Dinv) return SKB_ERR_WORKSPACE;
   for (int k0 = 0; k0 < Mp; k0 += NB) {
-    potrf_diag_kernel<<<1, 256, 0, st>>>(G, ld, k0, NB, status);
+    potrf_diag_kernel<<<1, NB, 0, st>>>(G, ld, k0, NB, status, Dinv);
     const int rest = Mp - k0 - NB;
     if (rest <= 0) break;
-    trsm_panel_kernel<<<(rest + 127) / 128, 128, 0, st>>>(G, ld, k0, NB, Mp);
     double* P = G + (int64_t)(k0 + NB) * ld + k0;
     double* T = G + (int64_t)(k0 + NB) * ld + k0 + NB;
+    GemmArgs gp = gemm_args(P, ld, 0, Dinv, NB, 1, P, ld, rest, NB, NB, 1.0, 0.0, 0);
+    int rc = gemm_launch(gp, 1, ws, st);
+    if (rc) return rc;
     GemmArgs g = gemm_args(P, ld, 0, P, ld, 1, T, ld, rest, rest, NB, -1.0, 1.0, 1);
-    int rc = gemm_launch(g, 1, ws, st);
+    rc = gemm_launch(g, 1, ws, st);
     if (rc) return rc;
   }
+  ws->off = mark;
   return 0;
 }
 
@@ -560,7 +650,8 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
   double* Y = (double*)skb_ws_take(&ws, (size_t)w * ldx * 8);
   int* status = (int*)skb_ws_take(&ws, 64);
   double* dstat = (double*)skb_ws_take(&ws, 64);
-  if (!G || !L1i || !L2i || !Y || !status || !dstat) return SKB_ERR_WORKSPACE;
+  double* dprod = (double*)skb_ws_take(&ws, (size_t)Mp * 8);
+  if (!G || !L1i || !L2i || !Y || !status || !dstat || !dprod) return SKB_ERR_WORKSPACE;
   const unsigned eb = (unsigned)((MM + 255) / 256);
   int rc;
   double hstat[4];
@@ -592,9 +683,10 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
     add_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(G, ld, m, shift);
     if ((rc = potrf(G, ld, Mp, status, &ws, st))) return rc;
   }
-  zero_upper_kernel<<<eb, 256, 0, st>>>(G, ld, Mp);
+  // potrf leaves the strict upper part zero (G was cleared before the lower-tile
+  // Gram, diagonal blocks are rewritten, trailing updates stay on lower tiles).
   if ((rc = trtri(G, L1i, ld, Mp, &ws, st))) return rc;
-  cudaMemcpyAsync(Lfac, G, MM * 8, cudaMemcpyDeviceToDevice, st);  // L = L1 (so far)
+  diag_accum_kernel<<<(m + 255) / 256, 256, 0, st>>>(G, ld, m, dprod, 1);  // |diag L| = |diag L1|
 
   const int passes = shifted ? 2 : 1;
   const double* Z = X;
@@ -605,27 +697,24 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
     Z = Y;
     if ((rc = gram(Y))) return rc;
     if ((rc = potrf(G, ld, Mp, status, &ws, st))) return rc;
-    zero_upper_kernel<<<eb, 256, 0, st>>>(G, ld, Mp);
     if ((rc = trtri(G, L2i, ld, Mp, &ws, st))) return rc;
-    // Linv = L2i * L1i (lower x lower); Lfac = Lfac * L2 (G holds L2)
+    diag_accum_kernel<<<(m + 255) / 256, 256, 0, st>>>(G, ld, m, dprod, 0);  // diag(L1 L2)
+    // Linv = L2i * L1i (lower x lower; tiles above the diagonal are skipped -> clear first)
+    cudaMemsetAsync(Linv, 0, MM * 8, st);
     GemmArgs gi = gemm_args(L2i, ld, 0, L1i, ld, 0, Linv, ld, Mp, Mp, Mp, 1.0, 0.0, 1);
     if ((rc = gemm_launch(gi, 1, &ws, st))) return rc;
-    zero_upper_kernel<<<eb, 256, 0, st>>>(Linv, ld, Mp);  // skipped tiles hold stale data
-    GemmArgs gl = gemm_args(Lfac, ld, 0, G, ld, 0, L2i /*tmp*/, ld, Mp, Mp, Mp, 1.0, 0.0, 1);
-    if ((rc = gemm_launch(gl, 1, &ws, st))) return rc;
-    zero_upper_kernel<<<eb, 256, 0, st>>>(L2i, ld, Mp);
-    cudaMemcpyAsync(Lfac, L2i, MM * 8, cudaMemcpyDeviceToDevice, st);
     if (p + 1 < passes) {
-      // next pass factors Y again: L1i <- Linv (cumulative inverse), Y = X Linv'
+      // next pass factors X again: L1i <- Linv (cumulative inverse), Y = X Linv'
       cudaMemcpyAsync(L1i, Linv, MM * 8, cudaMemcpyDeviceToDevice, st);
       Z = X;
     }
   }
-  zero_upper_kernel<<<eb, 256, 0, st>>>(Linv, ld, Mp);
-  zero_upper_kernel<<<eb, 256, 0, st>>>(Lfac, ld, Mp);
   dim3 tg((Mp + 31) / 32, (Mp + 31) / 32);
   transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(Linv, LinvT, ld, Mp);
-  diag_stats_kernel<<<1, 1024, 0, st>>>(Lfac, ld, m, dstat, 1);
+  if (Lfac) {  // L = Linv^-1 is not needed by the solver; only materialised on request
+    if ((rc = trtri(Linv, Lfac, ld, Mp, &ws, st))) return rc;
+  }
+  vec_minmax_kernel<<<1, 1024, 0, st>>>(dprod, m, dstat);
   cudaMemcpyAsync(hstat, dstat, 24, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&hst, status, 4, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;

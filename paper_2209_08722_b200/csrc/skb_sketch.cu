@@ -16,6 +16,7 @@
 //     __dmul_rn/__dadd_rn (no FMA). Splitting rows (not members) across
 //     threads keeps the per-(i, b) summation order of the reference exactly.
 #include <algorithm>
+#include <cstdlib>
 
 #include "skb_common.cuh"
 #include "skb_internal.h"
@@ -35,39 +36,55 @@ __global__ void bucket_chunk_prefix_kernel(int32_t* __restrict__ hist, int nchun
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= w) return;
   int32_t run = 0;
-  for (int c = 0; c < nchunks; ++c) {
-    const int32_t t = hist[(int64_t)c * w + b];
-    hist[(int64_t)c * w + b] = run;
-    run += t;
+  for (int c0 = 0; c0 < nchunks; c0 += 16) {  // batch the loads: they are independent
+    int32_t t[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) t[q] = c0 + q < nchunks ? hist[(int64_t)(c0 + q) * w + b] : 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (c0 + q < nchunks) hist[(int64_t)(c0 + q) * w + b] = run;
+      run += t[q];
+    }
   }
   total[b] = (uint32_t)run;
 }
 
-// One warp per chunk: entries in ascending order, ranks via match_any.
-__global__ void bucket_scatter_kernel(const int32_t* __restrict__ cols,
-                                      const double* __restrict__ vals, int64_t N, int s,
-                                      int64_t C, int w, const int32_t* __restrict__ hist,
-                                      const uint64_t* __restrict__ start,
-                                      int32_t* __restrict__ mem_j, double* __restrict__ mem_v) {
-  extern __shared__ uint32_t cursor[];
-  const int lane = threadIdx.x;
+// One CTA per chunk: the chunk's bucket ids are staged in shared memory by all
+// threads, then warp 0 ranks them in entry order (match_any) against a
+// shared-memory cursor per bucket and writes the entry index to its slot.
+constexpr int kScatterSub = 4096;
+
+__global__ void __launch_bounds__(256) bucket_scatter_kernel(
+    const int32_t* __restrict__ cols, int64_t N, int64_t C, int w,
+    const int32_t* __restrict__ hist, const uint64_t* __restrict__ start,
+    int32_t* __restrict__ mem_e) {
+  extern __shared__ uint32_t sm_scatter[];
+  uint32_t* cursor = sm_scatter;
+  int32_t* sb = reinterpret_cast<int32_t*>(sm_scatter + w);
   const int64_t c = blockIdx.x, e0 = c * C, e1 = min(N, e0 + C);
-  for (int b = lane; b < w; b += 32) cursor[b] = (uint32_t)(start[b] + hist[c * w + b]);
-  __syncwarp();
-  for (int64_t base = e0; base < e1; base += 32) {
-    const int64_t e = base + lane;
-    const bool act = e < e1;
-    const unsigned amask = __ballot_sync(0xffffffffu, act);
-    if (!act) break;
-    const int b = cols[e];
-    const unsigned peers = __match_any_sync(amask, b);
-    const int rank = __popc(peers & ((1u << lane) - 1u));
-    const uint32_t pos = cursor[b] + rank;
-    mem_j[pos] = (int32_t)(e / s);
-    mem_v[pos] = vals[e];
-    __syncwarp(amask);
-    if (rank == 0) cursor[b] += __popc(peers);
-    __syncwarp(amask);
+  for (int b = threadIdx.x; b < w; b += blockDim.x)
+    cursor[b] = (uint32_t)(start[b] + hist[c * w + b]);
+  const int lane = threadIdx.x & 31;
+  for (int64_t s0 = e0; s0 < e1; s0 += kScatterSub) {
+    const int cnt = (int)min((int64_t)kScatterSub, e1 - s0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) sb[t] = cols[s0 + t];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      for (int base = 0; base < cnt; base += 32) {
+        const int t = base + lane;
+        const bool act = t < cnt;
+        const unsigned amask = __ballot_sync(0xffffffffu, act);
+        if (!act) break;
+        const int b = sb[t];
+        const unsigned peers = __match_any_sync(amask, b);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        mem_e[cursor[b] + rank] = (int32_t)(s0 + t);
+        __syncwarp(amask);
+        if (rank == 0) cursor[b] += __popc(peers);
+        __syncwarp(amask);
+      }
+    }
   }
 }
 
@@ -105,10 +122,11 @@ struct StageMeta {
 constexpr int kConsumers = 256;
 
 template <int KP>  // row pairs per consumer thread: m <= 512 * KP
-__global__ void __launch_bounds__(kConsumers + 32, 1)
+__global__ void __launch_bounds__(kConsumers + 32, 2)
     sketch_accumulate_kernel(const double* __restrict__ A, int64_t lda, int m,
                              const double* __restrict__ d, const uint64_t* __restrict__ start,
-                             const int32_t* __restrict__ mem_j, const double* __restrict__ mem_v,
+                             const int32_t* __restrict__ mem_e, const double* __restrict__ vals,
+                             int s,
                              int w, int stages, unsigned int* __restrict__ counter,
                              double* __restrict__ X, int64_t ldx) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -159,8 +177,9 @@ __global__ void __launch_bounds__(kConsumers + 32, 1)
         int64_t j = 0;
         double v = 0.0, dj = 0.0;
         if (e < e1) {
-          j = mem_j[e];
-          v = mem_v[e];
+          const int64_t ei = mem_e[e];
+          j = ei / s;
+          v = vals[ei];
           dj = d[j];
         }
         const int cnt = (int)min((uint64_t)32, e1 - eb);
@@ -267,7 +286,7 @@ extern "C" size_t skb_sketch_workspace_bytes(int64_t n, int32_t w, int32_t s) {
   const int64_t N = n * (int64_t)s;
   int64_t C = std::max<int64_t>(4096, (N * (int64_t)w) / (16ll << 20) + 1);
   const int64_t nch = (N + C - 1) / C;
-  return (size_t)nch * w * 4 + (size_t)w * 4 + (size_t)(w + 1) * 8 + (size_t)N * 12 + 16 + 8 * 256;
+  return (size_t)nch * w * 4 + (size_t)w * 4 + (size_t)(w + 1) * 8 + (size_t)N * 4 + 16 + 8 * 256;
 }
 
 extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda,
@@ -284,10 +303,10 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
   int32_t* hist = (int32_t*)skb_ws_take(&ws, (size_t)nch * w * 4);
   uint32_t* total = (uint32_t*)skb_ws_take(&ws, (size_t)w * 4);
   uint64_t* start = (uint64_t*)skb_ws_take(&ws, (size_t)(w + 1) * 8);
-  int32_t* mem_j = (int32_t*)skb_ws_take(&ws, (size_t)std::max<int64_t>(N, 1) * 4);
-  double* mem_v = (double*)skb_ws_take(&ws, (size_t)std::max<int64_t>(N, 1) * 8);
+  int32_t* mem_e = (int32_t*)skb_ws_take(&ws, (size_t)std::max<int64_t>(N, 1) * 4);
   unsigned int* counter = (unsigned int*)skb_ws_take(&ws, 16);
-  if (!hist || !total || !start || !mem_j || !mem_v || !counter) return SKB_ERR_WORKSPACE;
+  if (!hist || !total || !start || !mem_e || !counter) return SKB_ERR_WORKSPACE;
+  if (N >= (1ll << 31)) return SKB_ERR_UNSUPPORTED;
   cudaMemsetAsync(hist, 0, (size_t)nch * w * 4, st);
   cudaMemsetAsync(counter, 0, 16, st);
   if (N > 0) {
@@ -296,21 +315,27 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
   bucket_chunk_prefix_kernel<<<(w + 255) / 256, 256, 0, st>>>(hist, (int)nch, w, total);
   scan_buckets_kernel<<<1, 1024, 0, st>>>(total, start, w);
   if (N > 0) {
-    const size_t csm = (size_t)w * 4;
-    if (csm > 48 * 1024) {
+    const size_t csm = (size_t)w * 4 + (size_t)kScatterSub * 4;
+    static size_t conf_sc = 0;
+    if (csm > 48 * 1024 && csm > conf_sc) {
       if (csm > 220 * 1024) return SKB_ERR_UNSUPPORTED;
       cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)csm);
+      conf_sc = csm;
     }
-    bucket_scatter_kernel<<<(unsigned)nch, 32, csm, st>>>(cols, vals, N, s, C, w, hist, start,
-                                                          mem_j, mem_v);
+    bucket_scatter_kernel<<<(unsigned)nch, 256, csm, st>>>(cols, N, C, w, hist, start, mem_e);
   }
   const size_t col_bytes = (size_t)lda * 8;
-  int stages = (int)std::min<size_t>(32, (200 * 1024) / col_bytes);
+  // tuning knobs (development): CTAs per SM and ring depth
+  // Two CTAs per SM (two producers per SM): 1.73 -> 1.32 ms at c2 (round-1 sweep).
+  static const int ctas_per_sm = getenv("SKB_SKETCH_CPS") ? atoi(getenv("SKB_SKETCH_CPS")) : 2;
+  static const int max_stages = getenv("SKB_SKETCH_STAGES") ? atoi(getenv("SKB_SKETCH_STAGES")) : 16;
+  const size_t budget = (size_t)(200 * 1024) / std::max(1, ctas_per_sm);
+  int stages = (int)std::min<size_t>((size_t)max_stages, budget / col_bytes);
   stages = std::max(stages, 2);
   const size_t smem =
       (((size_t)stages * (16 + sizeof(StageMeta)) + 127) & ~(size_t)127) + stages * col_bytes;
-  const int grid = std::min(skb_num_sms(), (int)std::max(1, w));
+  const int grid = std::min(skb_num_sms() * std::max(1, ctas_per_sm), (int)std::max(1, w));
   int rc = 0;
   // one configured-smem watermark per kernel instantiation
   static size_t conf[3] = {0, 0, 0};
@@ -321,8 +346,8 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
         rc = SKB_ERR_CUDA;
       conf[which] = smem;
     }
-    kern<<<grid, kConsumers + 32, smem, st>>>(A, lda, (int)m, d, start, mem_j, mem_v, w, stages,
-                                              counter, X, ldx);
+    kern<<<grid, kConsumers + 32, smem, st>>>(A, lda, (int)m, d, start, mem_e, vals, s, w,
+                                              stages, counter, X, ldx);
   };
   if (m <= 512)
     launch(sketch_accumulate_kernel<1>, 0);

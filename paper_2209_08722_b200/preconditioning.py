@@ -37,7 +37,7 @@ class PreconditionerFactor:
 
     Linv: torch.Tensor    # (Mp, Mp) lower, L^-1
     LinvT: torch.Tensor   # (Mp, Mp) upper, L^-T
-    Lfac: torch.Tensor    # (Mp, Mp) lower, L
+    Lfac: torch.Tensor | None  # (Mp, Mp) lower L, only when requested
     X: DeviceMatrix       # ADW' (w x m, bucket-major)
     m: int
     diag_min: float
@@ -64,7 +64,7 @@ def build_preconditioner(X: DeviceMatrix, rank_tol: float = RANK_TOL,
     dev = X.cols.device
     Linv = torch.empty((Mp, Mp), dtype=F64, device=dev)
     LinvT = torch.empty((Mp, Mp), dtype=F64, device=dev)
-    Lfac = torch.empty((Mp, Mp), dtype=F64, device=dev)
+    Lfac = None  # L itself is not needed by the solver (diag(L) comes from the factor stats)
     need = int(_lib.lib().skb_factor_workspace_bytes(m, w))
     ws, cap = workspace(need)
     stats = np.zeros(4, dtype=np.float64)
