@@ -25,9 +25,12 @@ SUM, MAX, MIN = "sum", "max", "min"
 class Comm:
     def __init__(self, group=None):
         self.group = group
+        self.host_staging = False
         if dist is not None and dist.is_available() and dist.is_initialized():
             self.rank = dist.get_rank(group)
             self.world = dist.get_world_size(group)
+            # gloo (CPU tests, shared-GPU emulation) reduces through host copies
+            self.host_staging = dist.get_backend(group) == "gloo"
         else:
             self.rank, self.world = 0, 1
 
@@ -42,7 +45,12 @@ class Comm:
     def allreduce_(self, t: torch.Tensor, op: str = SUM) -> torch.Tensor:
         if self.world > 1:
             rop = {SUM: dist.ReduceOp.SUM, MAX: dist.ReduceOp.MAX, MIN: dist.ReduceOp.MIN}[op]
-            dist.all_reduce(t, op=rop, group=self.group)
+            if self.host_staging and t.is_cuda:
+                h = t.cpu()
+                dist.all_reduce(h, op=rop, group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=rop, group=self.group)
         return t
 
     def combine_(self, vals: torch.Tensor, ops) -> torch.Tensor:
@@ -66,11 +74,12 @@ class Comm:
             return t
         sizes = [shard_range(n, r, self.world) for r in range(self.world)]
         width = max(j1 - j0 for j0, j1 in sizes)
-        buf = torch.zeros(width, dtype=t.dtype, device=t.device)
+        dev = "cpu" if self.host_staging else t.device
+        buf = torch.zeros(width, dtype=t.dtype, device=dev)
         buf[: t.numel()].copy_(t)
         out = [torch.empty_like(buf) for _ in range(self.world)]
         dist.all_gather(out, buf, group=self.group)
-        return torch.cat([o[: j1 - j0] for o, (j0, j1) in zip(out, sizes)])
+        return torch.cat([o[: j1 - j0] for o, (j0, j1) in zip(out, sizes)]).to(t.device)
 
     def barrier(self):
         if self.world > 1:
