@@ -122,7 +122,7 @@ struct StageMeta {
 constexpr int kConsumers = 256;
 
 template <int KP>  // row pairs per consumer thread: m <= 512 * KP
-__global__ void __launch_bounds__(kConsumers + 32, 2)
+__global__ void __launch_bounds__(kConsumers + 32, KP <= 4 ? 2 : 1)
     sketch_accumulate_kernel(const double* __restrict__ A, int64_t lda, int m,
                              const double* __restrict__ d, const uint64_t* __restrict__ start,
                              const int32_t* __restrict__ mem_e, const double* __restrict__ vals,
@@ -294,7 +294,7 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
                                 int32_t s, int32_t w, double* X, int64_t ldx, void* workspace,
                                 size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (m < 1 || m > 2048 || lda < m || (lda & 1) || ldx < m || (ldx & 1) || s < 1 || w < 1)
+  if (m < 1 || m > 16384 || lda < m || (lda & 1) || ldx < m || (ldx & 1) || s < 1 || w < 1)
     return SKB_ERR_ARG;
   skb_ws ws = skb_ws_make(workspace, ws_bytes);
   const int64_t N = n * (int64_t)s;
@@ -328,7 +328,8 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
   const size_t col_bytes = (size_t)lda * 8;
   // tuning knobs (development): CTAs per SM and ring depth
   // Two CTAs per SM (two producers per SM): 1.73 -> 1.32 ms at c2 (round-1 sweep).
-  static const int ctas_per_sm = getenv("SKB_SKETCH_CPS") ? atoi(getenv("SKB_SKETCH_CPS")) : 2;
+  static const int cps_env = getenv("SKB_SKETCH_CPS") ? atoi(getenv("SKB_SKETCH_CPS")) : 2;
+  const int ctas_per_sm = m <= 2048 ? cps_env : 1;  // large m: one CTA (register budget)
   static const int max_stages = getenv("SKB_SKETCH_STAGES") ? atoi(getenv("SKB_SKETCH_STAGES")) : 16;
   const size_t budget = (size_t)(200 * 1024) / std::max(1, ctas_per_sm);
   int stages = (int)std::min<size_t>((size_t)max_stages, budget / col_bytes);
@@ -338,7 +339,7 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
   const int grid = std::min(skb_num_sms() * std::max(1, ctas_per_sm), (int)std::max(1, w));
   int rc = 0;
   // one configured-smem watermark per kernel instantiation
-  static size_t conf[3] = {0, 0, 0};
+  static size_t conf[6] = {0, 0, 0, 0, 0, 0};
   auto launch = [&](auto kern, int which) {
     if (smem > conf[which]) {
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -353,8 +354,14 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
     launch(sketch_accumulate_kernel<1>, 0);
   else if (m <= 1024)
     launch(sketch_accumulate_kernel<2>, 1);
-  else
+  else if (m <= 2048)
     launch(sketch_accumulate_kernel<4>, 2);
+  else if (m <= 4096)
+    launch(sketch_accumulate_kernel<8>, 3);
+  else if (m <= 8192)
+    launch(sketch_accumulate_kernel<16>, 4);
+  else
+    launch(sketch_accumulate_kernel<32>, 5);
   if (rc) return rc;
   return skb_launch_status(__func__);
 }

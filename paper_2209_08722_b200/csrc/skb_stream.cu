@@ -17,6 +17,7 @@
 // in a fixed order per CTA, then across CTAs by skb_reduce_partials: the
 // result is deterministic run to run.
 #include <algorithm>
+#include <cstdlib>
 
 #include "skb_common.cuh"
 #include "skb_internal.h"
@@ -318,6 +319,129 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ----------------------------------------------------- CTA-cooperative variant
+// For m > 1024 (c3: m = 2000; any m up to 16384): the 256 threads of a CTA
+// split the ROWS of every column (thread t owns row pairs t + 256k), so
+// per-thread state stays small at any m. A stage holds cb consecutive
+// columns, filled by one cp.async.bulk issued by thread 0; the column dots
+// are reduced across the CTA through shared memory (fixed order), then every
+// thread applies the rank-cb update to its rows. Two barriers per stage.
+constexpr int kCoopThreads = 256;
+constexpr int kCoopMaxCb = 8;
+
+template <int KP, class Op>
+__global__ void __launch_bounds__(kCoopThreads, KP <= 8 ? 2 : 1)
+    colcoop_kernel(const double* __restrict__ A, int64_t lda, int m, int64_t n, int cb,
+                   int stages, int64_t ngroups, const double* __restrict__ z,
+                   double* __restrict__ part, Op op, const int* __restrict__ gate) {
+  if (gate && *gate) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int NW = kCoopThreads / 32;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  double* red = reinterpret_cast<double*>(smem + 256);         // [NW][kCoopMaxCb]
+  double* prev = red + NW * kCoopMaxCb;                        // [kCoopMaxCb][6]
+  unsigned char* bufs = smem + 256 + 8 * (NW * kCoopMaxCb + kCoopMaxCb * 6);
+  bufs = reinterpret_cast<unsigned char*>(((uintptr_t)bufs + 127) & ~(uintptr_t)127);
+  const size_t col_bytes = (size_t)lda * 8, stage_bytes = (size_t)cb * col_bytes;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  double zr[2 * KP], acc[2 * KP];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int r = 512 * k + 2 * tid + e;
+      zr[2 * k + e] = (Op::kDot && r < m) ? z[r] : 0.0;
+      acc[2 * k + e] = 0.0;
+    }
+  }
+  __syncthreads();
+  const int64_t G = gridDim.x;
+  const int64_t my = (int64_t)blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / G + 1 : 0;
+  const uint64_t pol = l2_evict_first_policy();
+  auto issue = [&](int64_t i, int st) {
+    const int64_t c0 = ((int64_t)blockIdx.x + i * G) * cb;
+    const int cnt = (int)min((int64_t)cb, n - c0);
+    const uint32_t bytes = (uint32_t)(cnt * col_bytes);
+    mbar_arrive_expect_tx(&full[st], bytes);
+    bulk_g2s(bufs + st * stage_bytes, A + c0 * lda, bytes, &full[st], pol);
+  };
+  if (tid == 0)
+    for (int64_t i = 0; i < min((int64_t)stages, my); ++i) issue(i, (int)i);
+  for (int64_t i = 0; i < my; ++i) {
+    const int st = (int)(i % stages);
+    const uint32_t ph = (uint32_t)((i / stages) & 1);
+    const int64_t c0 = ((int64_t)blockIdx.x + i * G) * cb;
+    const int cnt = (int)min((int64_t)cb, n - c0);
+    if (tid < cnt) {
+      Pre p;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) p.v[q] = 0.0;
+      op.load(c0 + tid, p);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) prev[tid * 6 + q] = p.v[q];
+    }
+    mbar_wait(&full[st], ph);
+    const double* buf = reinterpret_cast<const double*>(bufs + st * stage_bytes);
+    if (Op::kDot) {
+      for (int c = 0; c < cnt; ++c) {
+        const double* col = buf + (size_t)c * lda;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const int r = 512 * k + 2 * tid;
+          if (r < m) {
+            const double2 a = *reinterpret_cast<const double2*>(col + r);
+            d0 = fma(a.x, zr[2 * k], d0);
+            d1 = fma(r + 1 < m ? a.y : 0.0, zr[2 * k + 1], d1);
+          }
+        }
+        const double s = warp_sum(d0 + d1);
+        if (lane == 0) red[warp * kCoopMaxCb + c] = s;
+      }
+    }
+    __syncthreads();
+    for (int c = 0; c < cnt; ++c) {
+      double dot = 0.0;
+      if (Op::kDot) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) dot += red[w * kCoopMaxCb + c];
+      }
+      Pre pc;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) pc.v[q] = prev[c * 6 + q];
+      const double cf = op.coef(c0 + c, pc, dot);
+      if (tid == c) op.emit(c0 + c, pc, dot, cf);
+      if (Op::kAxpy) {
+        const double* col = buf + (size_t)c * lda;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const int r = 512 * k + 2 * tid;
+          if (r < m) {
+            const double2 a = *reinterpret_cast<const double2*>(col + r);
+            acc[2 * k] = fma(cf, a.x, acc[2 * k]);
+            acc[2 * k + 1] = fma(cf, r + 1 < m ? a.y : 0.0, acc[2 * k + 1]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // stage, red and prev are free
+    if (tid == 0 && i + stages < my) issue(i + stages, st);
+  }
+  if (!Op::kAxpy) return;
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int r = 512 * k + 2 * tid + e;
+      if (r < m) part[(size_t)blockIdx.x * m + r] = acc[2 * k + e];
+    }
+  }
+}
+
 // out[i] = sum_b part[b][i] (fixed order: 8 interleaved slices, combined in order) - sub[i]
 __global__ void reduce_partials_kernel(const double* __restrict__ part, int nb, int m,
                                        const double* __restrict__ sub, double* __restrict__ out,
@@ -365,6 +489,46 @@ static StreamCfg stream_cfg(int m, int64_t n, int64_t lda) {
   return c;
 }
 
+constexpr int kCoopMaxM = 16384;
+
+static StreamCfg coop_cfg(int m, int64_t n, int64_t lda) {
+  StreamCfg c;
+  const size_t col_bytes = (size_t)lda * 8;
+  c.cb = (int)std::max<size_t>(1, std::min<size_t>(kCoopMaxCb, 32768 / col_bytes));
+  const size_t stage_bytes = (size_t)c.cb * col_bytes;
+  const size_t head = 256 + 8 * (8 * kCoopMaxCb + kCoopMaxCb * 6) + 128;
+  // CTAs per SM: the CTA runs its stages in lockstep, so a second resident CTA
+  // overlaps one CTA's reduction latency with the other's streaming.
+  static const int cps_env = getenv("SKB_COOP_CPS") ? atoi(getenv("SKB_COOP_CPS")) : 2;
+  const int cps = m > 4096 ? 1 : cps_env;  // KP > 8 instantiations are 1 CTA/SM
+  const size_t budget = (size_t)(200 * 1024) / (size_t)std::max(1, cps);
+  c.stages = (int)std::max<size_t>(2, std::min<size_t>(8, budget / stage_bytes));
+  while (c.stages > 2 && head + c.stages * stage_bytes > 225 * 1024) --c.stages;
+  c.nw = kCoopThreads / 32;
+  c.smem = head + (size_t)c.stages * stage_bytes;
+  c.ngroups = (n + c.cb - 1) / c.cb;
+  c.grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)skb_num_sms() * std::max(1, cps), c.ngroups));
+  return c;
+}
+
+template <int KP, class Op>
+static int launch_coop(const StreamCfg& c, const double* A, int64_t lda, int m, int64_t n,
+                       const double* z, double* part, const Op& op, cudaStream_t st,
+                       const int* gate) {
+  auto kern = colcoop_kernel<KP, Op>;
+  static size_t configured = 0;
+  if (c.smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) !=
+        cudaSuccess)
+      return SKB_ERR_CUDA;
+    configured = c.smem;
+  }
+  kern<<<c.grid, kCoopThreads, c.smem, st>>>(A, lda, m, n, c.cb, c.stages, c.ngroups, z, part, op,
+                                             gate);
+  return 0;
+}
+
 template <int R2, bool ZREG, class Op>
 static int launch_r2(const StreamCfg& c, const double* A, int64_t lda, int m, int64_t n,
                      const double* z, double* part, const Op& op, cudaStream_t st,
@@ -391,7 +555,7 @@ static int run_stream(const double* A, int64_t lda, int m, int64_t n, const doub
                       cudaStream_t st, const int* gate = nullptr, double* part_ext = nullptr,
                       int* nparts_out = nullptr) {
   if (m < 1 || n < 0 || lda < m || (lda & 1) || ((uintptr_t)A & 15)) return SKB_ERR_ARG;
-  if (m > 2048) return SKB_ERR_UNSUPPORTED;
+  if (m > kCoopMaxM) return SKB_ERR_UNSUPPORTED;
   if (n == 0) {
     if (nparts_out) *nparts_out = 0;
     if (Op::kAxpy && !part_ext) {
@@ -403,7 +567,7 @@ static int run_stream(const double* A, int64_t lda, int m, int64_t n, const doub
     }
     return 0;
   }
-  const StreamCfg c = stream_cfg(m, n, lda);
+  const StreamCfg c = m > 1024 ? coop_cfg(m, n, lda) : stream_cfg(m, n, lda);
   double* part = part_ext;
   if (Op::kAxpy && !part) {
     part = (double*)skb_ws_take(ws, (size_t)c.grid * m * 8);
@@ -411,7 +575,16 @@ static int run_stream(const double* A, int64_t lda, int m, int64_t n, const doub
   }
   if (nparts_out) *nparts_out = c.grid;
   int rc;
-  if (m <= 64)
+  if (m > 1024) {
+    if (m <= 2048)
+      rc = launch_coop<4>(c, A, lda, m, n, z, part, op, st, gate);
+    else if (m <= 4096)
+      rc = launch_coop<8>(c, A, lda, m, n, z, part, op, st, gate);
+    else if (m <= 8192)
+      rc = launch_coop<16>(c, A, lda, m, n, z, part, op, st, gate);
+    else
+      rc = launch_coop<32>(c, A, lda, m, n, z, part, op, st, gate);
+  } else if (m <= 64)
     rc = launch_r2<1, true>(c, A, lda, m, n, z, part, op, st, gate);
   else if (m <= 128)
     rc = launch_r2<2, true>(c, A, lda, m, n, z, part, op, st, gate);
@@ -419,10 +592,8 @@ static int run_stream(const double* A, int64_t lda, int m, int64_t n, const doub
     rc = launch_r2<4, true>(c, A, lda, m, n, z, part, op, st, gate);
   else if (m <= 512)
     rc = launch_r2<8, true>(c, A, lda, m, n, z, part, op, st, gate);
-  else if (m <= 1024)
-    rc = launch_r2<16, true>(c, A, lda, m, n, z, part, op, st, gate);
   else
-    rc = launch_r2<32, false>(c, A, lda, m, n, z, part, op, st, gate);
+    rc = launch_r2<16, true>(c, A, lda, m, n, z, part, op, st, gate);
   if (rc) return rc;
   if (Op::kAxpy && !part_ext)
     reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, c.grid, m, sub, out, gate);
@@ -514,5 +685,5 @@ extern "C" int skb_reduce_partials(const double* part, int32_t nparts, int64_t m
 }
 
 extern "C" size_t skb_stream_workspace_bytes(int64_t m) {
-  return (size_t)skb_num_sms() * (size_t)m * 8 + 256;
+  return (size_t)4 * skb_num_sms() * (size_t)m * 8 + 256;  // up to 4 partials per SM
 }
