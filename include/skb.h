@@ -183,6 +183,27 @@ int skb_pcg_step_a(const double* q, const double* Aq, double* dy, double* r, int
 int skb_pcg_step_b(const double* r, const double* z, double* q, int64_t m, int32_t t_max,
                    void* state, double* trace, void* stream);
 
+/* Chebyshev iteration (krylov_solvers.py:108-153) on the same state: after
+ * skb_pcg_init and z = Q^-1 r, skb_cheb_init (tol < 0: run the full schedule);
+ * per step k: skb_cheb_step_q (q = z | z + beta q; dy += alpha q), the normal
+ * apply Aq = A D^2 A' q, skb_cheb_step_r (r -= alpha Aq), z = Q^-1 r,
+ * skb_cheb_trace. alpha_k, beta_k come from the fixed band (host scalars). */
+int skb_cheb_init(const double* r, const double* z, int64_t m, double tol, void* state,
+                  double* trace, void* stream);
+int skb_cheb_step_q(const double* z, double* q, double* dy, int64_t m, double alpha, double beta,
+                    int32_t first, void* state, void* stream);
+int skb_cheb_step_r(double* r, const double* Aq, int64_t m, double alpha, void* state,
+                    void* stream);
+int skb_cheb_trace(const double* r, const double* z, int64_t m, int32_t t_max, void* state,
+                   double* trace, void* stream);
+
+/* Direct solver pieces (krylov_solvers.py:156-171): G = A diag(w) A' (lower
+ * tiles, DMMA), transpose, identity padding of a factor matrix. */
+int skb_weighted_gram(const double* A, int64_t m, int64_t n, int64_t lda, const double* wts,
+                      double* G, int64_t ldg, void* workspace, size_t ws_bytes, void* stream);
+int skb_transpose(const double* S, double* D, int64_t ld, int32_t n, void* stream);
+int skb_set_identity_pad(double* G, int64_t ld, int32_t m, int32_t Mp, void* stream);
+
 /* Whole single-device PCG, one synchronisation. vec: 5*ldv doubles scratch.
  * out_host = {iterations, converged, status bits}; trace_host: iterations+1. */
 int skb_pcg_solve(const double* A, int64_t m, int64_t n, int64_t lda, const double* d2,

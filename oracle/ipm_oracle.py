@@ -194,6 +194,84 @@ def pcg(op, f: Factor, p, t_max: int, tol: float):
     return dy, norms, its, False
 
 
+def chebyshev(op, f: Factor, p, zeta, t_max, tol=None):
+    """krylov_solvers.py:108-153 -> (dy, residual_norms, iterations, converged)."""
+    if not 0.0 < zeta <= 1.0:
+        raise OracleError("InvalidZeta")
+    lo, hi = 2.0 / (2.0 + zeta), 2.0 / (2.0 - zeta)
+    d0, c = 0.5 * (hi + lo), 0.5 * (hi - lo)
+    dy = np.zeros(op.m)
+    r = p.copy()
+    z = f.inv(r)
+    norms = [float(np.sqrt(max(r @ z, 0.0)))]
+    if norms[0] == 0.0:
+        return dy, norms, 0, True
+    target = tol * norms[0] if tol is not None else None
+    a = 0.0
+    q = np.zeros(op.m)
+    its = 0
+    for k in range(t_max):
+        if k == 0:
+            q = z.copy()
+            a = 1.0 / d0
+        else:
+            bt = (0.5 if k == 1 else 0.25) * (c * a) ** 2
+            a = 1.0 / (d0 - bt / a)
+            q = z + bt * q
+        dy += a * q
+        r -= a * op.apply(q)
+        z = f.inv(r)
+        norms.append(float(np.sqrt(max(r @ z, 0.0))))
+        its += 1
+        if target is not None and norms[-1] <= target:
+            return dy, norms, its, True
+    return dy, norms, its, target is None
+
+
+def unpreconditioned_cg(op, p, t_max, tol):
+    """krylov_solvers.py:174-204."""
+    dy = np.zeros(op.m)
+    r = p.copy()
+    norms = [float(np.linalg.norm(r))]
+    if norms[0] == 0.0:
+        return dy, norms, 0, True
+    target = tol * norms[0]
+    gam = float(r @ r)
+    q = r.copy()
+    its = 0
+    for _ in range(t_max):
+        Aq = op.apply(q)
+        curv = float(q @ Aq)
+        if curv <= 0:
+            raise OracleError("Breakdown", f"curvature {curv:.3e}")
+        a = gam / curv
+        dy += a * q
+        r -= a * Aq
+        gnew = float(r @ r)
+        norms.append(float(np.sqrt(gnew)))
+        its += 1
+        if norms[-1] <= target:
+            return dy, norms, its, True
+        q = r + (gnew / gam) * q
+        gam = gnew
+    return dy, norms, its, False
+
+
+def direct_solve(op, p, cap=2000):
+    """krylov_solvers.py:156-171 (dense Cholesky + one refinement)."""
+    import scipy.linalg
+    if op.m > cap:
+        raise OracleError("TooLarge")
+    M = (op.A.multiply(op.d2[None, :]) @ op.A.T).toarray()
+    try:
+        cho = scipy.linalg.cho_factor(M, lower=True, check_finite=False)
+    except scipy.linalg.LinAlgError as exc:
+        raise OracleError("NotPositiveDefinite", str(exc))
+    dy = scipy.linalg.cho_solve(cho, p, check_finite=False)
+    dy += scipy.linalg.cho_solve(cho, p - op.apply(dy), check_finite=False)
+    return dy
+
+
 # ------------------------------------------------------------- correction
 
 
@@ -365,10 +443,11 @@ class Params:
 
     def __init__(self, mode="infeasible", gamma=0.5, sigma=0.5, zeta=0.5, sketch="sparse",
                  w=None, s=None, tol_cg=1e-5, tol_outer=1e-9, seed=0, max_outer=200,
-                 t_max=None):
+                 t_max=None, solver="pcg", correction=True):
         self.mode, self.gamma, self.sigma, self.zeta = mode, gamma, sigma, zeta
         self.sketch, self.w, self.s, self.tol_cg = sketch, w, s, tol_cg
         self.tol_outer, self.seed, self.max_outer, self.t_max = tol_outer, seed, max_outer, t_max
+        self.solver, self.correction = solver, correction
 
     @property
     def delta(self):
@@ -416,46 +495,77 @@ def ipm_step(A, b, c, it, prm, rng, r0_norm=None, mu0=None, a_scale=None, trace_
     p_norm = float(np.linalg.norm(p))
     t_base = prm.t_max if prm.t_max is not None else default_t_max(A.shape[1], prm.sigma,
                                                                      prm.gamma, prm.zeta)
-    w, s_nnz = auto_sketch_dims(A.shape[0], A.shape[1], prm.delta)
-    if prm.w is not None:
-        w = prm.w
-    if prm.s is not None:
-        s_nnz = prm.s
+    tol_eff = prm.tol_cg
+    if not prm.correction or prm.solver == "unpreconditioned":      # ipm_core.py:436-448
+        if mode == "infeasible":
+            budget = 0.05 * (it.mu / mu0) * r0_norm
+        else:
+            budget = 0.05 * FEAS_TOL * (1.0 + float(np.linalg.norm(b))) / max(prm.max_outer, 1)
+        tol_eff = max(min(prm.tol_cg, budget / max(p_norm, 1e-300)), 1e-14)
+        t_deep = math.ceil(math.log(1.0 / tol_eff) / math.log(1.0 / prm.zeta)) + 2
+        t_base = max(t_base, t_deep)
     W = f = None
     seed = None
+    w = 0
     rank_retries = v_retries = inner_total = 0
-    best = chosen = None
-    sched = [(True, t_base), (False, 2 * t_base)] + [(True, 2 * t_base)] * 3
-    for fresh, t_eff in sched:
-        if fresh or W is None:
-            W, f, rr = build_factor(A, d, prm, rng, w, s_nnz)
-            rank_retries += rr
-            seed = W.seed
-        dy, norms, its, conv = pcg(op, f, p, t_eff, prm.tol_cg)
-        if trace_hook is not None:
-            trace_hook(W, f, dy, norms)
-        inner_total += its
-        infeas = op.apply(dy) - p
-        scale = float(np.linalg.norm(infeas)) + p_norm
-        v, inv_res = compute_v(f, W, it.x, it.s, infeas, scale if scale > 0 else 1.0)
-        vnorm = float(np.linalg.norm(v))
-        slack = float(np.sqrt(3.0 * A.shape[1] * it.mu) * norms[-1] - vnorm)
-        cand = (dy, norms, its, v, vnorm, slack, infeas)
-        if vnorm <= prm.gamma * prm.sigma * it.mu / 4.0:
-            chosen = cand
-            break
-        v_retries += 1
-        if best is None or vnorm < best[4]:
-            best = cand
-    if chosen is None:
-        chosen = best
-    dy, norms, its, v, vnorm, slack, infeas = chosen
+    v = infeas = None
+    vnorm, slack = 0.0, float("nan")
+    if prm.solver == "direct":                                         # ipm_core.py:450-453
+        dy = direct_solve(op, p)
+        norms, its = [p_norm, float(np.linalg.norm(op.apply(dy) - p))], 0
+    elif prm.solver == "unpreconditioned":                             # ipm_core.py:454-456
+        dy, norms, its, conv = unpreconditioned_cg(op, p, max(1000, 20 * A.shape[0]), tol_eff)
+        inner_total = its
+    else:
+        w, s_nnz = auto_sketch_dims(A.shape[0], A.shape[1], prm.delta)
+        if prm.w is not None:
+            w = prm.w
+        if prm.s is not None:
+            s_nnz = prm.s
+        best = chosen = None
+        sched = [(True, t_base), (False, 2 * t_base)] + [(True, 2 * t_base)] * 3
+        for fresh, t_eff in sched:
+            if fresh or W is None:
+                W, f, rr = build_factor(A, d, prm, rng, w, s_nnz)
+                rank_retries += rr
+                seed = W.seed
+            if prm.solver == "chebyshev":
+                dy, norms, its, conv = chebyshev(op, f, p, prm.zeta, t_eff,
+                                                 None if prm.correction else tol_eff)
+            else:
+                dy, norms, its, conv = pcg(op, f, p, t_eff, tol_eff)
+            if trace_hook is not None:
+                trace_hook(W, f, dy, norms)
+            inner_total += its
+            if not prm.correction:
+                chosen = (dy, norms, its, None, 0.0, float("nan"), None)
+                break
+            infeas = op.apply(dy) - p
+            scale = float(np.linalg.norm(infeas)) + p_norm
+            v, inv_res = compute_v(f, W, it.x, it.s, infeas, scale if scale > 0 else 1.0)
+            vnorm = float(np.linalg.norm(v))
+            slack = float(np.sqrt(3.0 * A.shape[1] * it.mu) * norms[-1] - vnorm)
+            cand = (dy, norms, its, v, vnorm, slack, infeas)
+            if vnorm <= prm.gamma * prm.sigma * it.mu / 4.0:
+                chosen = cand
+                break
+            v_retries += 1
+            if best is None or vnorm < best[4]:
+                best = cand
+        if chosen is None:
+            chosen = best
+        dy, norms, its, v, vnorm, slack, infeas = chosen
 
-    scale = float(np.linalg.norm(infeas)) + p_norm
-    v_inv = float(np.linalg.norm(np.asarray(A @ (v / it.s)) - infeas)) / max(scale, 1e-300)
-    if v_inv > V_INVARIANT_TOL:
-        raise OracleError("InvariantViolated", f"correction invariant {v_inv:.3e}")
-    dx, ds, cross = assemble_directions(A, b, it, dy, v, prm.sigma, mode, a_scale)
+    v_inv = float("nan")
+    if v is not None:
+        scale = float(np.linalg.norm(infeas)) + p_norm
+        v_inv = float(np.linalg.norm(np.asarray(A @ (v / it.s)) - infeas)) / max(scale, 1e-300)
+        if v_inv > V_INVARIANT_TOL:
+            raise OracleError("InvariantViolated", f"correction invariant {v_inv:.3e}")
+    else:
+        v = np.zeros(A.shape[1])
+    strict = prm.solver == "direct" or v_inv == v_inv
+    dx, ds, cross = assemble_directions(A, b, it, dy, v, prm.sigma, mode, a_scale, strict)
     at = max_alpha(A, b, c, it, dx, dy, ds, prm.gamma, mode, r0_norm, mu0)
     ab = argmin_alpha(it, dx, ds, cross, at)
     new = make_iterate(A, b, c, it.x + ab * dx, it.y + ab * dy, it.s + ab * ds, it.k + 1)
@@ -472,7 +582,7 @@ def ipm_step(A, b, c, it, prm, rng, r0_norm=None, mu0=None, a_scale=None, trace_
         raise OracleError("InvariantViolated", "linear mu identity")
     if new.mu > it.mu * (1.0 + 1e-12):
         raise OracleError("InvariantViolated", "mu increased")
-    v_ok = vnorm <= prm.gamma * prm.sigma * it.mu / 4.0
+    v_ok = v_inv == v_inv and vnorm <= prm.gamma * prm.sigma * it.mu / 4.0
     if mode == "feasible" and v_ok:
         if new.mu > (1.0 - 0.5 * ab * (1.0 - 1.25 * prm.sigma)) * it.mu * (1.0 + 1e-10):
             raise OracleError("InvariantViolated", "mu decrease bound")
@@ -487,7 +597,8 @@ def ipm_step(A, b, c, it, prm, rng, r0_norm=None, mu0=None, a_scale=None, trace_
         alpha_bar=float(ab), inner_iterations=its, inner_iterations_total=inner_total,
         f_norm0=float(norms[0]), f_norm=float(norms[-1]), v_norm=vnorm, v_bar=v_bar,
         v_invariant_rel=v_inv, v_norm_slack=slack, v_ok=bool(v_ok), v_retries=v_retries,
-        rank_retries=rank_retries, sketch_w=w, sketch_seed=seed,
+        rank_retries=rank_retries, sketch_w=w if prm.solver in ("pcg", "chebyshev") else 0,
+        sketch_seed=seed,
         residual_ratio=float(new.residual_norm / max(r0_norm, 1e-300))
         if r0_norm is not None else float("nan"),
         mu_identity_error=float(mu_err), clip_count=clip_count,

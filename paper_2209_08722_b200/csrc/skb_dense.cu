@@ -42,6 +42,7 @@ struct GemmArgs {
   int splits, kchunk;
   double alpha, beta;
   int ta, tb, lower_only;
+  const double* kscale;  // optional: opA(i,k) *= kscale[k] (weighted SYRK A diag(w) A')
 };
 
 SKB_DEV void dmma(double (&c)[2], double a, double b) {
@@ -86,7 +87,10 @@ __global__ void __launch_bounds__(128) dgemm_kernel(GemmArgs g) {
       }
       const int gi = i0 + ii, gk = k0 + kk;
       double v = 0.0;
-      if (gi < g.M && gk < k_end) v = g.ta ? A[(int64_t)gk * g.lda + gi] : A[(int64_t)gi * g.lda + gk];
+      if (gi < g.M && gk < k_end) {
+        v = g.ta ? A[(int64_t)gk * g.lda + gi] : A[(int64_t)gi * g.lda + gk];
+        if (g.kscale) v *= g.kscale[gk];
+      }
       ra[e] = v;
       int kb, jj;
       if (g.tb) {
@@ -539,6 +543,29 @@ extern "C" int skb_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K,
   g.sB = strideB;
   g.sC = strideC;
   return gemm_launch(g, std::max(1, batch), &ws, (cudaStream_t)stream);
+}
+
+// G = A diag(w) A' (lower tiles) for column-major A (n columns of lda): the
+// normal matrix of the direct solver (krylov_solvers.py:50, NormalOperator.dense).
+extern "C" int skb_weighted_gram(const double* A, int64_t m, int64_t n, int64_t lda,
+                                 const double* wts, double* G, int64_t ldg, void* workspace,
+                                 size_t ws_bytes, void* stream) {
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  GemmArgs g = gemm_args(A, lda, 1, A, lda, 0, G, ldg, (int)m, (int)m, (int)n, 1.0, 0.0, 1);
+  g.kscale = wts;
+  return gemm_launch(g, 1, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_transpose(const double* S, double* D, int64_t ld, int32_t n, void* stream) {
+  dim3 tg((n + 31) / 32, (n + 31) / 32);
+  transpose_kernel<<<tg, dim3(32, 8), 0, (cudaStream_t)stream>>>(S, D, ld, n);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_set_identity_pad(double* G, int64_t ld, int32_t m, int32_t Mp, void* stream) {
+  set_identity_pad_kernel<<<(unsigned)(((int64_t)Mp * Mp + 255) / 256), 256, 0,
+                            (cudaStream_t)stream>>>(G, ld, m, Mp);
+  return skb_launch_status(__func__);
 }
 
 static int round_pad(int m) {

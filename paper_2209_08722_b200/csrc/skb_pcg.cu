@@ -122,9 +122,101 @@ __global__ void pcg_step_b_kernel(const double* __restrict__ r, const double* __
   if (threadIdx.x == 0) S->gamma = gn;
 }
 
+// ---- Chebyshev (krylov_solvers.py:108-153): alpha/beta come from the fixed
+// eigenvalue band, so the host passes them per step; only r'z is reduced.
+
+// init after z = Q^-1 p: norm0 = sqrt(max(r'z, 0)), target = tol*norm0 (tol < 0: none)
+__global__ void cheb_init_kernel(const double* __restrict__ r, const double* __restrict__ z,
+                                 int m, double tol, PcgState* S, double* trace) {
+  __shared__ double buf[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) s = fma(r[i], z[i], s);
+  const double g = block_sum(s, buf);
+  if (threadIdx.x == 0) {
+    const double n0 = sqrt(fmax(g, 0.0));
+    S->norm0 = n0;
+    trace[0] = n0;
+    S->target = tol >= 0.0 ? tol * n0 : -1.0;
+    if (n0 == 0.0) {
+      S->converged = 1;
+      S->stop = 1;
+    }
+  }
+}
+
+// q = z (first) or z + beta q; dy += alpha q
+__global__ void cheb_q_kernel(const double* __restrict__ z, double* __restrict__ q,
+                              double* __restrict__ dy, int m, double alpha, double beta, int first,
+                              const PcgState* S) {
+  if (S->stop) return;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double qi = first ? z[i] : __dadd_rn(z[i], __dmul_rn(beta, q[i]));
+    q[i] = qi;
+    dy[i] = __dadd_rn(dy[i], __dmul_rn(alpha, qi));
+  }
+}
+
+// r -= alpha Aq
+__global__ void cheb_r_kernel(double* __restrict__ r, const double* __restrict__ Aq, int m,
+                              double alpha, const PcgState* S) {
+  if (S->stop) return;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) r[i] = __dsub_rn(r[i], __dmul_rn(alpha, Aq[i]));
+}
+
+// trace sqrt(max(r'z, 0)); stop on target or t_max
+__global__ void cheb_trace_kernel(const double* __restrict__ r, const double* __restrict__ z, int m,
+                                  int t_max, PcgState* S, double* trace) {
+  __shared__ double buf[32];
+  if (S->stop) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) s = fma(r[i], z[i], s);
+  const double g = block_sum(s, buf);
+  if (threadIdx.x == 0) {
+    const double nrm = sqrt(fmax(g, 0.0));
+    const int it = S->iters + 1;
+    trace[it] = nrm;
+    S->iters = it;
+    if (S->target >= 0.0 && nrm <= S->target) {
+      S->converged = 1;
+      S->stop = 1;
+    } else if (it >= t_max) {
+      S->stop = 1;
+      if (S->target < 0.0) S->converged = 1;  // no tolerance: the full schedule "converges"
+    }
+  }
+}
+
 }  // namespace skb
 
 using namespace skb;
+
+extern "C" int skb_cheb_init(const double* r, const double* z, int64_t m, double tol, void* state,
+                             double* trace, void* stream) {
+  cheb_init_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(r, z, (int)m, tol, (PcgState*)state,
+                                                         trace);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_cheb_step_q(const double* z, double* q, double* dy, int64_t m, double alpha,
+                               double beta, int32_t first, void* state, void* stream) {
+  cheb_q_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(z, q, dy, (int)m, alpha, beta, first,
+                                                      (const PcgState*)state);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_cheb_step_r(double* r, const double* Aq, int64_t m, double alpha, void* state,
+                               void* stream) {
+  cheb_r_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(r, Aq, (int)m, alpha,
+                                                      (const PcgState*)state);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_cheb_trace(const double* r, const double* z, int64_t m, int32_t t_max,
+                              void* state, double* trace, void* stream) {
+  cheb_trace_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(r, z, (int)m, t_max, (PcgState*)state,
+                                                          trace);
+  return skb_launch_status(__func__);
+}
 
 extern "C" size_t skb_pcg_state_bytes(void) { return sizeof(PcgState); }
 

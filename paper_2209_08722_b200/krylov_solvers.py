@@ -153,6 +153,136 @@ def _pcg_generic(op, f, p, dy, t_max, tol, B):
     return iters, conv, status
 
 
+def _state_result(B):
+    st = B.state.view(torch.int32)[8:12].cpu().numpy()
+    iters, conv, status = int(st[2]), int(st[3]), int(st[1])
+    B.trace_host[:iters + 1] = B.trace[:iters + 1].cpu().numpy()
+    return iters, conv, status
+
+
+def _apply_step(op, q, Aq, stop_ptr, state_view):
+    """Aq = op(q): gated device launch for NormalOperator, host-checked otherwise.
+    Returns False when a foreign operator's loop should end (state stopped)."""
+    if isinstance(op, NormalOperator):
+        op.apply(q, out=Aq, gate=_Ptr(stop_ptr))
+        return True
+    if int(state_view[8].item()):
+        return False
+    Aq.copy_(op.apply(q))
+    return True
+
+
+def chebyshev(op, f: PreconditionerFactor, p: torch.Tensor, zeta: float, t_max: int,
+              tol: float | None = None):
+    """Chebyshev iteration on the fixed band [2/(2+zeta), 2/(2-zeta)]
+    (krylov_solvers.py:108-153). Returns (dy, SolverTrace)."""
+    from .errors import InvalidZeta
+    if not 0.0 < zeta <= 1.0:
+        raise InvalidZeta(f"zeta must lie in (0, 1], got {zeta}")
+    lam_min = 2.0 / (2.0 + zeta)
+    lam_max = 2.0 / (2.0 - zeta)
+    d0 = 0.5 * (lam_max + lam_min)
+    c = 0.5 * (lam_max - lam_min)
+    m = op.m
+    t_max = int(t_max)
+    B = _buffers(m, t_max, p.device)
+    dy = torch.empty(m, dtype=F64, device=p.device)
+    r, z, q, Aq, t = (B.v(k) for k in range(5))
+    sp_ = stream_ptr()
+    stop_ptr = B.state.data_ptr() + 32
+    state_view = B.state.view(torch.int32)
+    _lib.call("skb_pcg_init", p, r, dy, m, B.state, sp_)
+    apply_inv(f, r, out=z, tmp=t)
+    _lib.call("skb_cheb_init", r, z, m, float(tol) if tol is not None else -1.0, B.state,
+              B.trace, sp_)
+    alpha = 0.0
+    for k in range(t_max):
+        if k == 0:
+            alpha, beta = 1.0 / d0, 0.0
+        else:
+            beta = (0.5 if k == 1 else 0.25) * (c * alpha) ** 2
+            alpha = 1.0 / (d0 - beta / alpha)
+        _lib.call("skb_cheb_step_q", z, q, dy, m, alpha, beta, 1 if k == 0 else 0, B.state, sp_)
+        if not _apply_step(op, q, Aq, stop_ptr, state_view):
+            break
+        _lib.call("skb_cheb_step_r", r, Aq, m, alpha, B.state, sp_)
+        _lib.call("skb_rowdot_gemv", f.Linv, f.ld, m, m, 1, r, t, _Ptr(stop_ptr), sp_)
+        _lib.call("skb_rowdot_gemv", f.LinvT, f.ld, m, m, 2, t, z, _Ptr(stop_ptr), sp_)
+        _lib.call("skb_cheb_trace", r, z, m, t_max, B.state, B.trace, sp_)
+    iters, conv, _ = _state_result(B)
+    if tol is None:
+        conv = 1
+    norms = [float(v) for v in B.trace_host[:iters + 1]]
+    return dy, SolverTrace(residual_norms=norms, iterations=iters, converged=bool(conv),
+                           zeta=zeta, t_max=t_max)
+
+
+def unpreconditioned_cg(op, p: torch.Tensor, t_max: int, tol: float):
+    """Plain CG baseline; the trace holds ||r|| (krylov_solvers.py:174-204).
+    The PCG kernels run with z aliased to r (M = I)."""
+    m = op.m
+    t_max = int(t_max)
+    B = _buffers(m, t_max, p.device)
+    dy = torch.empty(m, dtype=F64, device=p.device)
+    r, _, q, Aq, _ = (B.v(k) for k in range(5))
+    sp_ = stream_ptr()
+    stop_ptr = B.state.data_ptr() + 32
+    state_view = B.state.view(torch.int32)
+    _lib.call("skb_pcg_init", p, r, dy, m, B.state, sp_)
+    _lib.call("skb_pcg_init2", r, r, q, m, float(tol), B.state, B.trace, sp_)
+    for _ in range(t_max):
+        if not _apply_step(op, q, Aq, stop_ptr, state_view):
+            break
+        _lib.call("skb_pcg_step_a", q, Aq, dy, r, m, B.state, sp_)
+        _lib.call("skb_pcg_step_b", r, r, q, m, t_max, B.state, B.trace, sp_)
+    iters, conv, status = _state_result(B)
+    _raise_status(status, "unpreconditioned_cg")
+    norms = [float(v) for v in B.trace_host[:iters + 1]]
+    return dy, SolverTrace(residual_norms=norms, iterations=iters, converged=bool(conv),
+                           t_max=t_max)
+
+
+DIRECT_CAP = 2000
+
+
+def direct_solve(op: "NormalOperator", p: torch.Tensor, cap: int = DIRECT_CAP) -> torch.Tensor:
+    """Dense Cholesky of A D^2 A' with one refinement pass (krylov_solvers.py:156-171):
+    DMMA weighted Gram, blocked device Cholesky, triangular inverse."""
+    from .errors import NotPositiveDefinite, TooLarge
+    m = op.m
+    if m > cap:
+        raise TooLarge(f"m={m} exceeds direct-solve cap {cap}")
+    lp = op.lp
+    Mp = int(_lib.lib().skb_factor_padded_dim(m))
+    dev = p.device
+    G = torch.zeros((Mp, Mp), dtype=F64, device=dev)
+    ws, cap_b = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, m)))
+    _lib.call("skb_weighted_gram", lp.A.cols, m, lp.A.n, lp.A.lda, op._d2, G, Mp, ws, cap_b,
+              stream_ptr())
+    if lp.comm.active:
+        lp.comm.allreduce_(G)
+    _lib.call("skb_set_identity_pad", G, Mp, m, Mp, stream_ptr())
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("skb_potrf", G, Mp, Mp, status, ws, cap_b, stream_ptr())
+    if int(status.item()) & 4:
+        raise NotPositiveDefinite("Cholesky of the normal matrix failed")
+    Linv = torch.empty_like(G)
+    _lib.call("skb_trtri", G, Linv, Mp, Mp, ws, cap_b, stream_ptr())
+    LinvT = torch.empty_like(G)
+    _lib.call("skb_transpose", Linv, LinvT, Mp, Mp, stream_ptr())
+
+    class _F:  # the two-gemv Q^-1 application on the exact normal matrix
+        pass
+    fac = _F()
+    fac.Linv, fac.LinvT, fac.m = Linv, LinvT, m
+    dy = apply_inv(fac, p)
+    resid = op.apply(dy)
+    _lib.call("skb_sub", p, resid, resid, m, stream_ptr())   # resid = p - A D^2 A' dy
+    corr = apply_inv(fac, resid)
+    _lib.call("skb_axpy", dy, 1.0, corr, dy, m, stream_ptr())
+    return dy
+
+
 class _Ptr:
     """A raw device address passed through _lib.call as a pointer."""
 

@@ -147,8 +147,39 @@ def small_traces():
         json.dump(res, f)
 
 
+def solver_traces():
+    """The other inner solvers (krylov_solvers.py:108-204) and correction off, on the
+    small LP in feasible mode (ipm_core.py:436-456)."""
+    res = {}
+    lpd = wide_dense_lp(40, 3000, 5)
+    lp = skipm.make_lp(lpd.A, lpd.b, lpd.c, name=lpd.name)
+    # Chebyshev's fixed band needs a certified embedding: w = 1200, s = 12 (at w = 4m it
+    # stalls for 200 outer steps in the reference too).
+    cases = {"chebyshev": dict(solver="chebyshev", w=1200, s=12),
+             "unpreconditioned": dict(solver="unpreconditioned", w=160, s=4),
+             "direct": dict(solver="direct", w=160, s=4),
+             "pcg_nocorr": dict(solver="pcg", correction=False, w=160, s=4)}
+    for name, kw in cases.items():
+        start = ipm_core.make_iterate(lp, lpd.x0, lpd.y0, lpd.s0)
+        prm = ipm_core.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5,
+                                 tol_outer=1e-6, seed=5, **kw)
+        try:
+            rep = ipm_core.solve(lp, start, prm)
+        except skipm.MaxIterations as e:
+            rep = e.report
+        d = rep.to_dict()
+        d.pop("params")
+        res[name] = d
+        print(f"{name}: outer {rep.outer} conv {rep.converged} inner {rep.sum_inner} "
+              f"obj {rep.objective!r}")
+    with open(os.path.join(HERE, "solver_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["hashes", "adw", "small", "c1"]
+    what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers"]
+    if "solvers" in what:
+        solver_traces()
     if "hashes" in what:
         hashes()
     if "adw" in what:

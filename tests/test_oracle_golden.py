@@ -146,3 +146,22 @@ def test_config1_trace(s_nnz):
     prm = O.Params(mode="feasible", gamma=gold["gamma_run"], sigma=0.5, w=400, s=s_nnz,
                    tol_outer=1e-6, seed=0)
     _compare_solve(O.solve(A, lpd.b, lpd.c, st, prm), gold[f"s{s_nnz}"], 1e-12)
+
+
+@pytest.mark.parametrize("name", ["chebyshev", "unpreconditioned", "direct", "pcg_nocorr"])
+def test_other_solvers_traces(name):
+    with open(os.path.join(GOLDEN, "solver_traces.json")) as f:
+        gold = json.load(f)[name]
+    kw = {"chebyshev": dict(solver="chebyshev", w=1200, s=12),
+          "unpreconditioned": dict(solver="unpreconditioned", w=160, s=4),
+          "direct": dict(solver="direct", w=160, s=4),
+          "pcg_nocorr": dict(solver="pcg", correction=False, w=160, s=4)}[name]
+    lpd, A = _oracle_problem(40, 3000, 5)
+    st = O.make_iterate(A, lpd.b, lpd.c, lpd.x0, lpd.y0, lpd.s0)
+    prm = O.Params(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5, tol_outer=1e-6, seed=5,
+                   **kw)
+    rep = O.solve(A, lpd.b, lpd.c, st, prm)
+    assert rep["outer"] == gold["outer"]
+    assert [r["inner_iterations"] for r in rep["steps"]] == gold["inner_iterations"]
+    np.testing.assert_allclose(rep["mu_trace"], gold["mu_trace"], rtol=1e-12)
+    assert abs(rep["objective"] - gold["objective"]) <= 1e-10 * abs(gold["objective"])
