@@ -247,6 +247,19 @@ int skb_crossing(const double* x, const double* s, const double* dx, const doubl
 int skb_vec_stats(const double* a, const double* sub, int64_t n, double* out, void* workspace,
                   size_t ws_bytes, void* stream);
 
+/* feasible_start pieces (ipm_core.py:814-969):
+ * skb_ratio_min: out = {min over dv<0 of -v/dv, min over dw<0 of -w/dw} (inf if none);
+ * skb_centering_grid: for 8 step lengths alphas[k], prod = (x + a dx)(s + a ds),
+ *   out[3k..3k+2] = {min prod, sum prod, count(prod <= 0)};
+ * skb_zero_col_fill: x[j] = 1 for every all-zero column of A. */
+int skb_ratio_min(const double* v, const double* dv, const double* w, const double* dw,
+                  int64_t n, double* out, void* workspace, size_t ws_bytes, void* stream);
+int skb_centering_grid(const double* x, const double* s, const double* dx, const double* ds,
+                       const double* alphas, int64_t n, double* out, void* workspace,
+                       size_t ws_bytes, void* stream);
+int skb_zero_col_fill(const double* A, int64_t m, int64_t n, int64_t lda, double* x,
+                      void* stream);
+
 /* y = x + alpha d;  out = a - b. */
 int skb_axpy(const double* x, double alpha, const double* d, double* y, int64_t n, void* stream);
 int skb_sub(const double* a, const double* b, double* out, int64_t n, void* stream);

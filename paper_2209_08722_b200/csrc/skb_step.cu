@@ -188,6 +188,69 @@ __global__ void __launch_bounds__(kRedThreads)
   grid_reduce<4>(v, ops, part, ticket, out);
 }
 
+// ---- feasible_start centering step (ipm_core.py:914-969)
+
+// out = {min over dv<0 of (-v)/dv (inf if none), min over dw<0 of (-w)/dw}
+__global__ void __launch_bounds__(kRedThreads)
+    ratio_min_kernel(const double* __restrict__ v, const double* __restrict__ dv,
+                     const double* __restrict__ w, const double* __restrict__ dw, int64_t n,
+                     double* part, unsigned* ticket, double* out) {
+  double r[2] = {INFINITY, INFINITY};
+  const int ops[2] = {R_MIN, R_MIN};
+  for (int64_t j = gtid(); j < n; j += gstride()) {
+    if (dv[j] < 0.0) r[0] = fmin(r[0], (-v[j]) / dv[j]);
+    if (dw[j] < 0.0) r[1] = fmin(r[1], (-w[j]) / dw[j]);
+  }
+  grid_reduce<2>(r, ops, part, ticket, out);
+}
+
+// For K step lengths a_k: prod = (x + a dx)(s + a ds); out[3k..3k+2] =
+// {min prod, sum prod, count(prod <= 0)} (theta = min/mean in the reference).
+constexpr int kGridK = 8;
+__global__ void __launch_bounds__(kRedThreads)
+    centering_grid_kernel(const double* __restrict__ x, const double* __restrict__ s,
+                          const double* __restrict__ dx, const double* __restrict__ ds,
+                          const double* __restrict__ alphas, int64_t n, double* part,
+                          unsigned* ticket, double* out) {
+  double v[3 * kGridK];
+  int ops[3 * kGridK];
+  double a[kGridK];
+#pragma unroll
+  for (int k = 0; k < kGridK; ++k) {
+    v[3 * k] = INFINITY;
+    v[3 * k + 1] = 0.0;
+    v[3 * k + 2] = 0.0;
+    ops[3 * k] = R_MIN;
+    ops[3 * k + 1] = R_SUM;
+    ops[3 * k + 2] = R_SUM;
+    a[k] = alphas[k];
+  }
+  for (int64_t j = gtid(); j < n; j += gstride()) {
+    const double xj = x[j], sj = s[j], dxj = dx[j], dsj = ds[j];
+#pragma unroll
+    for (int k = 0; k < kGridK; ++k) {
+      const double p = (xj + a[k] * dxj) * (sj + a[k] * dsj);
+      v[3 * k] = fmin(v[3 * k], p);
+      v[3 * k + 1] += p;
+      v[3 * k + 2] += p <= 0.0 ? 1.0 : 0.0;
+    }
+  }
+  grid_reduce<3 * kGridK>(v, ops, part, ticket, out);
+}
+
+// x[j] = 1 for every all-zero column j of A (phase1_point pins them, ipm_core.py:834-835).
+__global__ void zero_col_fill_kernel(const double* __restrict__ A, int64_t lda, int m, int64_t n,
+                                     double* __restrict__ x) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const double* col = A + j * lda;
+  int nz = 0;
+  for (int i = lane; i < m; i += 32) nz |= col[i] != 0.0;
+  nz = __any_sync(0xffffffffu, nz);
+  if (!nz && lane == 0) x[j] = 1.0;
+}
+
 // y = x + alpha * d   (numpy: it.y + a * dirn.dy)
 __global__ void axpy_kernel(const double* __restrict__ x, double alpha,
                             const double* __restrict__ d, double* __restrict__ y, int64_t n) {
@@ -212,7 +275,7 @@ static int red_grid(int64_t n) {
 
 // Reduction scratch: partials (grid * 16 doubles) + ticket.
 extern "C" size_t skb_reduce_workspace_bytes(void) {
-  return (size_t)2 * skb_num_sms() * 16 * 8 + 512;
+  return (size_t)2 * skb_num_sms() * 32 * 8 + 512;
 }
 
 #define RED_WS                                                                   \
@@ -267,6 +330,34 @@ extern "C" int skb_vec_stats(const double* a, const double* sub, int64_t n, doub
                              void* workspace, size_t ws_bytes, void* stream) {
   RED_WS;
   vec_stats_kernel<<<red_grid(n), kRedThreads, 0, st>>>(a, sub, n, part, ticket, out);
+  LAUNCH_OK;
+}
+
+extern "C" int skb_ratio_min(const double* v, const double* dv, const double* w, const double* dw,
+                             int64_t n, double* out, void* workspace, size_t ws_bytes,
+                             void* stream) {
+  RED_WS;
+  ratio_min_kernel<<<red_grid(n), kRedThreads, 0, st>>>(v, dv, w, dw, n, part, ticket, out);
+  LAUNCH_OK;
+}
+
+extern "C" int skb_centering_grid(const double* x, const double* s, const double* dx,
+                                  const double* ds, const double* alphas, int64_t n, double* out,
+                                  void* workspace, size_t ws_bytes, void* stream) {
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  unsigned* ticket = (unsigned*)skb_ws_take(&ws, 256);
+  double* part = (double*)skb_ws_take(&ws, (size_t)2 * skb_num_sms() * 3 * kGridK * 8);
+  if (!ticket || !part) return SKB_ERR_WORKSPACE;
+  centering_grid_kernel<<<red_grid(n), kRedThreads, 0, (cudaStream_t)stream>>>(
+      x, s, dx, ds, alphas, n, part, ticket, out);
+  LAUNCH_OK;
+}
+
+extern "C" int skb_zero_col_fill(const double* A, int64_t m, int64_t n, int64_t lda, double* x,
+                                 void* stream) {
+  if (n <= 0) return 0;
+  zero_col_fill_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      A, lda, (int)m, n, x);
   LAUNCH_OK;
 }
 

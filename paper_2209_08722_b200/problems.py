@@ -63,6 +63,22 @@ def wide_dense_lp(m: int, n: int, seed: int = 0) -> DenseLP:
     return DenseLP(A, b, c, x0, y0, s0, name=f"wide_dense_{m}x{n}_s{seed}")
 
 
+def random_feasible_dense(m: int, n: int, density: float, seed: int):
+    """The reference's random_feasible_lp instance (lp_model.py:134-160), same
+    draw order: mask, values, diagonal boost, x_feas, y0, slack. Returns dense
+    (A, b, c); used by the feasible-start parity tests (no start supplied)."""
+    g = np.random.Generator(np.random.Philox(int(seed)))
+    keep = g.random((m, n)) < density
+    A = np.where(keep, g.random((m, n)), 0.0)
+    k = min(m, n)
+    A[np.arange(k), np.arange(k)] += g.random(k)
+    x_feas = g.random(n) + 0.5
+    b = A @ x_feas
+    y0 = g.standard_normal(m)
+    c = A.T @ y0 + g.random(n) + 0.1
+    return A, b, c
+
+
 def ill_conditioned_lp(m: int, n: int, seed: int = 0) -> DenseLP:
     """config c5 with the repaired start of SURVEY.md Appendix C:
     A = diag(r) G, r log-uniform on [1e-3, 1e3]; x0, s0 ~ U(0.5, 1.5)."""

@@ -176,8 +176,34 @@ def solver_traces():
         json.dump(res, f)
 
 
+def start_traces():
+    """solve() with no start in feasible mode: phase 1 + shifted dual + centering
+    (ipm_core.py:814-969) on the reference's random_feasible_lp instance."""
+    from paper_2209_08722_b200.problems import random_feasible_dense
+    A, b, c = random_feasible_dense(20, 200, 0.5, 3)
+    ref_lp = skipm.random_feasible_lp(20, 200, 0.5, 3)
+    assert np.array_equal(ref_lp.A.toarray(), A) and np.array_equal(ref_lp.b, b)
+    res = {}
+    prm = ipm_core.IpmParams(mode="feasible", gamma=0.5, sigma=0.5, tol_outer=1e-6, seed=2)
+    x0, aux = ipm_core.phase1_point(ref_lp, prm)
+    res["phase1_x0"] = x0.tolist()
+    res["phase1_aux_outer"] = aux.outer
+    st = ipm_core.feasible_start(ref_lp, prm)
+    res["start"] = dict(x=st.x.tolist(), y=st.y.tolist(), s=st.s.tolist(), mu=st.mu)
+    rep = ipm_core.solve(ref_lp, None, prm)
+    d = rep.to_dict()
+    d.pop("params")
+    res["solve"] = d
+    print(f"feasible start: aux outer {aux.outer}, start mu {st.mu:.4e}, solve outer {rep.outer} "
+          f"obj {rep.objective!r}")
+    with open(os.path.join(HERE, "start_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers"]
+    what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers", "start"]
+    if "start" in what:
+        start_traces()
     if "solvers" in what:
         solver_traces()
     if "hashes" in what:

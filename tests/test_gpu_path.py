@@ -370,6 +370,33 @@ def test_config1_lockstep_s1(P):
     assert strict_steps >= 10
 
 
+def test_feasible_start_and_solve_without_start(P):
+    """solve(lp) in feasible mode with no start: phase 1 (infeasible-mode solve of
+    the auxiliary LP) + projection, shifted-objective dual, centering prelude,
+    mu shrink (ipm_core.py:814-969), all on the device, vs the reference."""
+    from paper_2209_08722_b200 import ipm_core as IC
+    from paper_2209_08722_b200.lp_model import LinearProgram
+    from paper_2209_08722_b200.problems import random_feasible_dense
+    with open(os.path.join(GOLDEN, "start_traces.json")) as f:
+        gold = json.load(f)
+    A, b, c = random_feasible_dense(20, 200, 0.5, 3)
+    lp = LinearProgram(sp.csr_matrix(A), b, c)
+    prm = IC.IpmParams(mode="feasible", gamma=0.5, sigma=0.5, tol_outer=1e-6, seed=2)
+    x0, aux = IC.phase1_point(lp, prm)
+    assert aux.outer == gold["phase1_aux_outer"]
+    g0 = np.array(gold["phase1_x0"])
+    assert np.max(np.abs(x0 - g0)) <= 1e-7 * np.max(np.abs(g0))
+    st = IC.feasible_start(lp, prm)
+    assert abs(st.mu - gold["start"]["mu"]) <= 1e-8 * gold["start"]["mu"]
+    gx = np.array(gold["start"]["x"])
+    assert np.max(np.abs(_h(st.x) - gx)) <= 1e-6 * np.max(np.abs(gx))
+    rep = IC.solve(lp, None, prm)
+    gs = gold["solve"]
+    assert rep.outer == gs["outer"] and [r.inner_iterations for r in rep.steps] == gs["inner_iterations"]
+    np.testing.assert_allclose(rep.mu_trace, gs["mu_trace"], rtol=1e-6)
+    assert abs(rep.objective - gs["objective"]) <= 1e-8 * abs(gs["objective"])
+
+
 @pytest.mark.parametrize("name", ["chebyshev", "unpreconditioned", "direct", "pcg_nocorr"])
 def test_other_solvers_trajectories(P, monkeypatch, name):
     """The device Chebyshev / plain CG / direct solvers and correction-off PCG
