@@ -137,6 +137,22 @@ int skb_sketch_gather(const int32_t* cols, const double* vals, int32_t s, int64_
                       const double* u, const double* x, const double* sv, double* v,
                       void* stream);
 
+/* ------------------------------------------------------ K9 Gaussian sketch --
+ * build_gaussian_sketch (sketching.py:131-139): W = standard_normal((n, w)) /
+ * sqrt(w) from Generator(Philox(seed)), bit-exact with numpy's ziggurat
+ * (tables taken from numpy's build). Writes draws [lo, count) (lo = 0,
+ * count = n*w: the whole W). Synchronises the stream.
+ * skb_gaussian_apply: X = (A diag(d) W)' (w x m) as one DMMA GEMM. */
+size_t skb_gaussian_workspace_bytes(int64_t count);
+int skb_gaussian_sketch(uint64_t key0, uint64_t key1, int64_t lo, int64_t count, int32_t w,
+                        double* W, void* workspace, size_t ws_bytes, void* stream);
+int skb_gaussian_apply(const double* A, int64_t m, int64_t n, int64_t lda, const double* d,
+                       const double* W, int32_t w, double* X, int64_t ldx, void* workspace,
+                       size_t ws_bytes, void* stream);
+/* v = sqrt(x .* s) .* t (compute_v for a dense or identity W, correction.py:58). */
+int skb_sqrt_xs_scale(const double* t, const double* x, const double* s, double* v, int64_t n,
+                      void* stream);
+
 /* ------------------------------------------------------- K3 factor (FP64) --
  * Replaces np.linalg.svd(ADW) (preconditioning.py:46). Factor matrices are
  * Mp x Mp row-major (Mp = skb_factor_padded_dim(m), identity-padded).

@@ -22,7 +22,9 @@ OBJ = os.path.join(HERE, "_build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                  "-I", os.path.join(ROOT, "include")]
+                  "-I", os.path.join(ROOT, "include"), "-I", OBJ]
+# generated at build time from numpy's own tables (see ziggurat_tables.py)
+ZIG_HEADER = os.path.join(OBJ, "skb_ziggurat_tables.h")
 # Elementwise step kernels follow numpy's rounding exactly: no FMA contraction.
 PER_FILE = {"skb_step.cu": ["-fmad=false"]}
 
@@ -43,7 +45,8 @@ def _stale(obj: str, src: str) -> bool:
         return True
     t = os.path.getmtime(obj)
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC)
-                    if f.endswith((".cuh", ".h"))] + [os.path.join(ROOT, "include", "skb.h")]
+                    if f.endswith((".cuh", ".h"))] + [os.path.join(ROOT, "include", "skb.h"),
+                                                      ZIG_HEADER]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -62,6 +65,9 @@ def _compile(src: str, verbose: bool) -> str:
 
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    sys.path.insert(0, HERE)
+    from ziggurat_tables import write_header
+    write_header(ZIG_HEADER)
     if force:
         for f in os.listdir(OBJ):
             os.remove(os.path.join(OBJ, f))

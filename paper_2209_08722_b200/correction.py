@@ -53,12 +53,10 @@ def compute_v(f: PreconditionerFactor, W: SketchOperator, x: torch.Tensor, s: to
         raise DimensionMismatch(f"infeas has shape {tuple(infeas.shape)}, expected ({f.m},)")
     u = apply_pinv_adw(f, infeas)
     v = torch.empty_like(x)
-    if W.kind == "identity":
-        # W u = u restricted to this rank's rows; v = sqrt(x s) * u
-        ul = u[W.j0:W.j0 + x.numel()].contiguous()
-        cols = torch.arange(x.numel(), dtype=torch.int32, device=x.device).view(-1, 1)
-        vals = torch.ones((x.numel(), 1), dtype=F64, device=x.device)
-        _lib.call("skb_sketch_gather", cols, vals, 1, x.numel(), ul, x, s, v, stream_ptr())
+    if W.kind in ("identity", "gaussian"):
+        # v = sqrt(x s) * (W u): W u is u's row slice (identity) or a dense gemv (Gaussian)
+        t = W.matvec(u)
+        _lib.call("skb_sqrt_xs_scale", t, x, s, v, x.numel(), stream_ptr())
     else:
         _lib.call("skb_sketch_gather", W.cols, W.vals, W.s, x.numel(), u, x, s, v, stream_ptr())
     # ||ADW u - infeas|| / denom   (correction.py:61-64)

@@ -556,6 +556,18 @@ extern "C" int skb_weighted_gram(const double* A, int64_t m, int64_t n, int64_t 
   return gemm_launch(g, 1, &ws, (cudaStream_t)stream);
 }
 
+// X = (A diag(d) W)' for a dense Gaussian W (n x w row-major): X[b][i] =
+// sum_j W[j][b] d_j A[i][j] as one DMMA GEMM (M = w, N = m, K = n) with the
+// column scaling fused into the operand load (sketching.py:158-159, K9).
+extern "C" int skb_gaussian_apply(const double* A, int64_t m, int64_t n, int64_t lda,
+                                  const double* d, const double* W, int32_t w, double* X,
+                                  int64_t ldx, void* workspace, size_t ws_bytes, void* stream) {
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  GemmArgs g = gemm_args(W, w, 1, A, lda, 0, X, ldx, w, (int)m, (int)n, 1.0, 0.0, 0);
+  g.kscale = d;
+  return gemm_launch(g, 1, &ws, (cudaStream_t)stream);
+}
+
 extern "C" int skb_transpose(const double* S, double* D, int64_t ld, int32_t n, void* stream) {
   dim3 tg((n + 31) / 32, (n + 31) / 32);
   transpose_kernel<<<tg, dim3(32, 8), 0, (cudaStream_t)stream>>>(S, D, ld, n);

@@ -251,6 +251,13 @@ __global__ void zero_col_fill_kernel(const double* __restrict__ A, int64_t lda, 
   if (!nz && lane == 0) x[j] = 1.0;
 }
 
+// v = sqrt(x s) * t   (correction.py:58 for a dense / identity W)
+__global__ void sqrt_xs_scale_kernel(const double* __restrict__ t, const double* __restrict__ x,
+                                     const double* __restrict__ s, double* __restrict__ v,
+                                     int64_t n) {
+  for (int64_t j = gtid(); j < n; j += gstride()) v[j] = sqrt(x[j] * s[j]) * t[j];
+}
+
 // y = x + alpha * d   (numpy: it.y + a * dirn.dy)
 __global__ void axpy_kernel(const double* __restrict__ x, double alpha,
                             const double* __restrict__ d, double* __restrict__ y, int64_t n) {
@@ -358,6 +365,12 @@ extern "C" int skb_zero_col_fill(const double* A, int64_t m, int64_t n, int64_t 
   if (n <= 0) return 0;
   zero_col_fill_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       A, lda, (int)m, n, x);
+  LAUNCH_OK;
+}
+
+extern "C" int skb_sqrt_xs_scale(const double* t, const double* x, const double* s, double* v,
+                                 int64_t n, void* stream) {
+  sqrt_xs_scale_kernel<<<red_grid(n), kRedThreads, 0, (cudaStream_t)stream>>>(t, x, s, v, n);
   LAUNCH_OK;
 }
 

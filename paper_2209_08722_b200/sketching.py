@@ -56,9 +56,11 @@ class SketchOperator:
             raise DimensionMismatch(f"u has shape {tuple(u.shape)}, expected ({self.w},)")
         if self.kind == "identity":
             return u[self.j0:self.j0 + self.n_local].clone()
-        if self.kind != "sparse_sign":
-            raise NotImplementedError("Gaussian sketch matvec is not on the B200 path yet")
         out = torch.empty(self.n_local, dtype=F64, device=u.device)
+        if self.kind == "gaussian":  # dense @ u, one warp per row (sketching.py:78-79)
+            _lib.call("skb_rowdot_gemv", self.dense, self.w, self.n_local, self.w, 0, u, out,
+                      None, stream_ptr())
+            return out
         _lib.call("skb_sketch_gather", self.cols, self.vals, self.s, self.n_local, u, None, None,
                   out, stream_ptr())
         return out
@@ -67,6 +69,8 @@ class SketchOperator:
     def n_local(self) -> int:
         if self.cols is not None:
             return int(self.cols.shape[0])
+        if self.dense is not None:
+            return int(self.dense.shape[0])
         return self.n if self.kind != "identity" else self._n_local
 
     _n_local: int = 0
@@ -110,12 +114,20 @@ def build_identity_sketch(n: int, rows=None) -> SketchOperator:
     return W
 
 
-def build_gaussian_sketch(n: int, w: int, seed: int) -> SketchOperator:
-    """Dense Gaussian sketch (sketching.py:131-139): SURVEY.md §8(f) item 3,
-    not yet on the B200 path."""
+def build_gaussian_sketch(n: int, w: int, seed: int, rows=None, device=None) -> SketchOperator:
+    """Dense Gaussian sketch (sketching.py:131-139): standard_normal((n, w)) / sqrt(w)
+    drawn on the GPU bit-exact with numpy's ziggurat (K9, csrc/skb_gauss.cu).
+    rows = (j0, j1) keeps this rank's row block (draws j0*w .. j1*w)."""
     if w < 1:
         raise InvalidDims(f"w must be positive, got {w}")
-    raise NotImplementedError("the Gaussian sketch (K9) is not implemented on the B200 path yet")
+    device = device or require_cuda()
+    j0, j1 = rows if rows is not None else (0, n)
+    k0, k1 = philox_key(seed)
+    dense = torch.empty((j1 - j0, w), dtype=F64, device=device)
+    need = int(_lib.lib().skb_gaussian_workspace_bytes(j1 * w))
+    ws, cap = workspace(need)
+    _lib.call("skb_gaussian_sketch", k0, k1, j0 * w, j1 * w, w, dense, ws, cap, stream_ptr())
+    return SketchOperator(kind="gaussian", n=n, w=w, s=0, seed=int(seed), dense=dense, j0=j0)
 
 
 def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = True):
@@ -143,8 +155,10 @@ def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = 
         ws, cap = workspace(need)
         _lib.call("skb_sketch_apply", A.cols, m, A.n, A.lda, d, W.cols, W.vals, W.s, W.w, X, ldx,
                   ws, cap, stream_ptr())
-    else:
-        raise NotImplementedError("Gaussian sketch apply (K9) is not implemented yet")
+    else:  # dense Gaussian: one DMMA GEMM, X = W' D A' (sketching.py:158-159)
+        ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, W.w)))
+        _lib.call("skb_gaussian_apply", A.cols, m, A.n, A.lda, d, W.dense, W.w, X, ldx, ws, cap,
+                  stream_ptr())
     if ldx != m:
         X[:, m:].zero_()
     if lp.comm.active:

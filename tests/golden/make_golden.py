@@ -176,6 +176,31 @@ def solver_traces():
         json.dump(res, f)
 
 
+def gaussian_traces():
+    """build_gaussian_sketch values (sketching.py:131-139) and Gaussian-sketch solves,
+    incl. the ill-conditioned c5 generator (repaired start)."""
+    from paper_2209_08722_b200.problems import ill_conditioned_lp
+    res = {"sketch": []}
+    for (n, w, seed) in [(3000, 64, 41), (100_000, 40, 42), (7, 3, 43)]:
+        W = sketching.build_gaussian_sketch(n, w, seed)
+        res["sketch"].append(dict(n=n, w=w, seed=seed, sha256=sha(W.dense),
+                                  head=W.dense.ravel()[:6].tolist(),
+                                  tail=W.dense.ravel()[-6:].tolist()))
+    for name, lpd in [("wide", wide_dense_lp(40, 3000, 5)), ("illcond", ill_conditioned_lp(30, 2000, 6))]:
+        lp = skipm.make_lp(lpd.A, lpd.b, lpd.c, name=lpd.name)
+        start = ipm_core.make_iterate(lp, lpd.x0, lpd.y0, lpd.s0)
+        prm = ipm_core.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1),
+                                 sigma=0.5 if name == "wide" else 0.3, sketch="gaussian",
+                                 w=4 * lpd.m, tol_outer=1e-6, seed=9)
+        rep = ipm_core.solve(lp, start, prm)
+        d = rep.to_dict()
+        d.pop("params")
+        res[name] = d
+        print(f"gaussian {name}: outer {rep.outer} inner {rep.sum_inner} obj {rep.objective!r}")
+    with open(os.path.join(HERE, "gaussian_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
 def start_traces():
     """solve() with no start in feasible mode: phase 1 + shifted dual + centering
     (ipm_core.py:814-969) on the reference's random_feasible_lp instance."""
@@ -201,7 +226,9 @@ def start_traces():
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers", "start"]
+    what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers", "start", "gaussian"]
+    if "gaussian" in what:
+        gaussian_traces()
     if "start" in what:
         start_traces()
     if "solvers" in what:

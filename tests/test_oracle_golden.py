@@ -148,6 +148,22 @@ def test_config1_trace(s_nnz):
     _compare_solve(O.solve(A, lpd.b, lpd.c, st, prm), gold[f"s{s_nnz}"], 1e-12)
 
 
+def test_gaussian_sketch_and_traces():
+    from paper_2209_08722_b200.problems import ill_conditioned_lp
+    with open(os.path.join(GOLDEN, "gaussian_traces.json")) as f:
+        gold = json.load(f)
+    for case in gold["sketch"]:
+        W = O.gaussian_sketch(case["n"], case["w"], case["seed"])
+        assert _sha(W) == case["sha256"]
+    for name, lpd in [("wide", wide_dense_lp(40, 3000, 5)), ("illcond", ill_conditioned_lp(30, 2000, 6))]:
+        A = sp.csr_matrix(lpd.A)
+        A.sort_indices()
+        st = O.make_iterate(A, lpd.b, lpd.c, lpd.x0, lpd.y0, lpd.s0)
+        prm = O.Params(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5 if name == "wide" else 0.3,
+                       sketch="gaussian", w=4 * lpd.m, tol_outer=1e-6, seed=9)
+        _compare_solve(O.solve(A, lpd.b, lpd.c, st, prm), gold[name], 1e-12)
+
+
 @pytest.mark.parametrize("name", ["chebyshev", "unpreconditioned", "direct", "pcg_nocorr"])
 def test_other_solvers_traces(name):
     with open(os.path.join(GOLDEN, "solver_traces.json")) as f:
