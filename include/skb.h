@@ -116,6 +116,45 @@ int skb_iterate(const double* A, int64_t m, int64_t n, int64_t lda, const double
 int skb_reduce_partials(const double* part, int32_t nparts, int64_t m, const double* sub,
                         double* out, void* stream);
 
+/* ---------------------------------------------- sparse A (CSC), config c4 --
+ * The same passes over A stored as CSC: colptr (int64, n+1), rowidx (int32),
+ * vals (double). One thread per column; z and the CTA's m-vector partial in
+ * shared memory (m <= 14080); partials reduced in a fixed order. */
+int skb_csc_normal_apply(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                         int64_t m, int64_t n, const double* d2, const double* z, double* u,
+                         const double* sub, const int* gate, void* workspace, size_t ws_bytes,
+                         void* stream);
+int skb_csc_gemv(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
+                 int64_t n, const double* x, double* u, const double* sub, void* workspace,
+                 size_t ws_bytes, void* stream);
+int skb_csc_gemv_ratio(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                       int64_t m, int64_t n, const double* v, const double* s, double* u,
+                       const double* sub, void* workspace, size_t ws_bytes, void* stream);
+int skb_csc_rhs(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
+                int64_t n, const double* x, const double* s, const double* r_d, double sigma_mu,
+                double* p, const double* r_p, void* workspace, size_t ws_bytes, void* stream);
+int skb_csc_gemv_t(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
+                   int64_t n, const double* y, const double* add, const double* sub, double* t,
+                   void* workspace, size_t ws_bytes, void* stream);
+int skb_csc_directions(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                       int64_t m, int64_t n, const double* dy, const double* x, const double* s,
+                       const double* v, const double* r_d, double sigma_mu, double* ds,
+                       double* dx, double* atdy, double* adx, void* workspace, size_t ws_bytes,
+                       void* stream);
+int skb_csc_iterate(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
+                    int64_t n, const double* x, const double* dx, const double* s,
+                    const double* ds, double alpha, const double* y_new, const double* b,
+                    const double* c, double* x_out, double* s_out, double* r_p, double* r_d,
+                    void* workspace, size_t ws_bytes, void* stream);
+/* Bit-exact ADW for CSC A (ascending-j sums per (row, bucket), no FMA). */
+int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx, const double* av,
+                         int64_t m, int64_t n, const double* d, const int32_t* cols,
+                         const double* vals, int32_t s, int32_t w, double* X, int64_t ldx,
+                         void* workspace, size_t ws_bytes, void* stream);
+/* Dense column-major copy (A zeroed by the caller). */
+int skb_csc_to_dense(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t n,
+                     double* A, int64_t lda, void* stream);
+
 /* ------------------------------------------------------------ K2 sketch --
  * X = (A diag(d) W)' for the sparse-sign W given by cols/vals (n x s), i.e.
  * X[b*ldx + i] = ADW[i, b] (bucket-major, w rows of length m). Bit-exact with

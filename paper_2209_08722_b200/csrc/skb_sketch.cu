@@ -289,22 +289,19 @@ extern "C" size_t skb_sketch_workspace_bytes(int64_t n, int32_t w, int32_t s) {
   return (size_t)nch * w * 4 + (size_t)w * 4 + (size_t)(w + 1) * 8 + (size_t)N * 4 + 16 + 8 * 256;
 }
 
-extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda,
-                                const double* d, const int32_t* cols, const double* vals,
-                                int32_t s, int32_t w, double* X, int64_t ldx, void* workspace,
-                                size_t ws_bytes, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  if (m < 1 || m > 16384 || lda < m || (lda & 1) || ldx < m || (ldx & 1) || s < 1 || w < 1)
-    return SKB_ERR_ARG;
-  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+// Stable counting sort of the n*s hash entries by bucket -> start[w+1], mem_e[N]
+// (entry indices, ascending within each bucket), plus a zeroed work counter.
+static int bucket_sort(const int32_t* cols, int64_t n, int32_t s, int32_t w, skb_ws* ws,
+                       cudaStream_t st, uint64_t** start_out, int32_t** mem_out,
+                       unsigned int** counter_out) {
   const int64_t N = n * (int64_t)s;
   const int64_t C = std::max<int64_t>(4096, (N * (int64_t)w) / (16ll << 20) + 1);
   const int64_t nch = (N + C - 1) / C;
-  int32_t* hist = (int32_t*)skb_ws_take(&ws, (size_t)nch * w * 4);
-  uint32_t* total = (uint32_t*)skb_ws_take(&ws, (size_t)w * 4);
-  uint64_t* start = (uint64_t*)skb_ws_take(&ws, (size_t)(w + 1) * 8);
-  int32_t* mem_e = (int32_t*)skb_ws_take(&ws, (size_t)std::max<int64_t>(N, 1) * 4);
-  unsigned int* counter = (unsigned int*)skb_ws_take(&ws, 16);
+  int32_t* hist = (int32_t*)skb_ws_take(ws, (size_t)nch * w * 4);
+  uint32_t* total = (uint32_t*)skb_ws_take(ws, (size_t)w * 4);
+  uint64_t* start = (uint64_t*)skb_ws_take(ws, (size_t)(w + 1) * 8);
+  int32_t* mem_e = (int32_t*)skb_ws_take(ws, (size_t)std::max<int64_t>(N, 1) * 4);
+  unsigned int* counter = (unsigned int*)skb_ws_take(ws, 16);
   if (!hist || !total || !start || !mem_e || !counter) return SKB_ERR_WORKSPACE;
   if (N >= (1ll << 31)) return SKB_ERR_UNSUPPORTED;
   cudaMemsetAsync(hist, 0, (size_t)nch * w * 4, st);
@@ -324,6 +321,118 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
       conf_sc = csm;
     }
     bucket_scatter_kernel<<<(unsigned)nch, 256, csm, st>>>(cols, N, C, w, hist, start, mem_e);
+  }
+  *start_out = start;
+  *mem_out = mem_e;
+  *counter_out = counter;
+  return 0;
+}
+
+// ---- CSC A (c4): one warp per bucket, the bucket's m-vector in shared memory.
+// Members are processed in ascending column order; a member's entries hit
+// distinct rows, so its (<= 32 at a time) lanes update without conflicts and
+// every (row, bucket) sum keeps scipy's ascending-j order, no FMA: bit-exact.
+constexpr int kCscStage = 8;  // entries staged per member (longer columns loop)
+
+__global__ void __launch_bounds__(32)
+    csc_sketch_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                      const double* __restrict__ av, int m, const double* __restrict__ d,
+                      const uint64_t* __restrict__ start, const int32_t* __restrict__ mem_e,
+                      const double* __restrict__ wvals, int s, int w,
+                      unsigned int* __restrict__ counter, double* __restrict__ X, int64_t ldx) {
+  extern __shared__ __align__(16) double sacc[];
+  int32_t* srow = reinterpret_cast<int32_t*>(sacc + m);
+  double* sval = reinterpret_cast<double*>(srow + 32 * kCscStage + 32);  // 8-aligned
+  sval = reinterpret_cast<double*>(((uintptr_t)sval + 15) & ~(uintptr_t)15);
+  const int lane = threadIdx.x;
+  for (;;) {
+    int b = 0;
+    if (lane == 0) b = (int)atomicAdd(counter, 1u);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (b >= w) break;
+    for (int i = lane; i < m; i += 32) sacc[i] = 0.0;
+    __syncwarp();
+    const uint64_t e0 = start[b], e1 = start[b + 1];
+    for (uint64_t eb = e0; eb < e1; eb += 32) {
+      const uint64_t e = eb + lane;
+      int64_t c0 = 0, cnt = 0;
+      double scl = 0.0, wv = 0.0;
+      if (e < e1) {
+        const int64_t ei = mem_e[e];
+        const int64_t j = ei / s;
+        wv = wvals[ei];
+        scl = d[j];
+        c0 = colptr[j];
+        cnt = colptr[j + 1] - c0;
+        for (int t = 0; t < kCscStage && t < cnt; ++t) {  // stage this member's entries
+          srow[lane * kCscStage + t] = rowidx[c0 + t];
+          sval[lane * kCscStage + t] = av[c0 + t];
+        }
+      }
+      __syncwarp();
+      const int nm = (int)min((uint64_t)32, e1 - eb);
+      for (int q = 0; q < nm; ++q) {
+        const int64_t cq = __shfl_sync(0xffffffffu, cnt, q);
+        const int64_t c0q = __shfl_sync(0xffffffffu, c0, q);
+        const double dq = __shfl_sync(0xffffffffu, scl, q);
+        const double wq = __shfl_sync(0xffffffffu, wv, q);
+        for (int64_t t = lane; t < cq; t += 32) {
+          const int r = t < kCscStage ? srow[q * kCscStage + t] : rowidx[c0q + t];
+          const double a = t < kCscStage ? sval[q * kCscStage + t] : av[c0q + t];
+          sacc[r] = __dadd_rn(sacc[r], __dmul_rn(__dmul_rn(a, dq), wq));
+        }
+        __syncwarp();
+      }
+    }
+    double* out = X + (int64_t)b * ldx;
+    for (int i = lane; i < m; i += 32) out[i] = sacc[i];
+    __syncwarp();
+  }
+}
+
+extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx,
+                                    const double* av, int64_t m, int64_t n, const double* d,
+                                    const int32_t* cols, const double* vals, int32_t s, int32_t w,
+                                    double* X, int64_t ldx, void* workspace, size_t ws_bytes,
+                                    void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < 1 || ldx < m || s < 1 || w < 1) return SKB_ERR_ARG;
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  uint64_t* start;
+  int32_t* mem_e;
+  unsigned int* counter;
+  int rc = bucket_sort(cols, n, s, w, &ws, st, &start, &mem_e, &counter);
+  if (rc) return rc;
+  const size_t smem = (size_t)m * 8 + 32 * kCscStage * 4 + 32 * 4 + 16 + 32 * kCscStage * 8;
+  if (smem > 220 * 1024) return SKB_ERR_UNSUPPORTED;
+  static size_t conf = 0;
+  if (smem > 48 * 1024 && smem > conf) {
+    if (cudaFuncSetAttribute(csc_sketch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return SKB_ERR_CUDA;
+    conf = smem;
+  }
+  const int per_sm = std::max(1, (int)((220 * 1024) / smem));
+  const int grid = std::min(skb_num_sms() * std::min(per_sm, 16), std::max(1, (int)w));
+  csc_sketch_kernel<<<grid, 32, smem, st>>>(colptr, rowidx, av, (int)m, d, start, mem_e, vals, s,
+                                            w, counter, X, ldx);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda,
+                                const double* d, const int32_t* cols, const double* vals,
+                                int32_t s, int32_t w, double* X, int64_t ldx, void* workspace,
+                                size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < 1 || m > 16384 || lda < m || (lda & 1) || ldx < m || (ldx & 1) || s < 1 || w < 1)
+    return SKB_ERR_ARG;
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  uint64_t* start;
+  int32_t* mem_e;
+  unsigned int* counter;
+  {
+    int rc0 = bucket_sort(cols, n, s, w, &ws, st, &start, &mem_e, &counter);
+    if (rc0) return rc0;
   }
   const size_t col_bytes = (size_t)lda * 8;
   // tuning knobs (development): CTAs per SM and ring depth

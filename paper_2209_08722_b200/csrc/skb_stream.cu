@@ -687,3 +687,165 @@ extern "C" int skb_reduce_partials(const double* part, int32_t nparts, int64_t m
 extern "C" size_t skb_stream_workspace_bytes(int64_t m) {
   return (size_t)4 * skb_num_sms() * (size_t)m * 8 + 256;  // up to 4 partials per SM
 }
+
+// ===================================================== sparse A (CSC), c4
+// The same Op family over a CSC matrix (colptr int64 n+1, rowidx int32, vals):
+// one thread per column (coalesced colptr/pre loads), z and the CTA's partial
+// m-vector in shared memory; the column dot gathers z, the update scatters
+// into the partial with shared-memory atomics. Per-CTA partials are reduced in
+// a fixed order as for the dense path; the order of additions inside a CTA
+// follows the hardware's atomic arbitration (tolerance parity, not bitwise).
+namespace skb {
+
+constexpr int kCscThreads = 512;
+
+template <class Op>
+__global__ void __launch_bounds__(kCscThreads)
+    csc_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+               const double* __restrict__ vals, int m, int64_t n, const double* __restrict__ z,
+               double* __restrict__ part, Op op, const int* __restrict__ gate) {
+  if (gate && *gate) return;
+  extern __shared__ __align__(16) double csm[];
+  double* zs = csm;
+  double* us = csm + (Op::kDot ? m : 0);
+  if (Op::kDot)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) zs[i] = z[i];
+  if (Op::kAxpy)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) us[i] = 0.0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    Pre p;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) p.v[q] = 0.0;
+    op.load(j, p);
+    const int64_t e0 = colptr[j], e1 = colptr[j + 1];
+    double dot = 0.0;
+    if (Op::kDot)
+      for (int64_t e = e0; e < e1; ++e) dot = fma(vals[e], zs[rowidx[e]], dot);
+    const double cf = op.coef(j, p, dot);
+    op.emit(j, p, dot, cf);
+    if (Op::kAxpy)
+      for (int64_t e = e0; e < e1; ++e) atomicAdd(&us[rowidx[e]], cf * vals[e]);
+  }
+  if (!Op::kAxpy) return;
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) part[(size_t)blockIdx.x * m + i] = us[i];
+}
+
+template <class Op>
+static int run_csc(const int64_t* colptr, const int32_t* rowidx, const double* vals, int m,
+                   int64_t n, const double* z, double* out, const double* sub, const Op& op,
+                   skb_ws* ws, cudaStream_t st, const int* gate = nullptr) {
+  if (m < 1 || n < 0) return SKB_ERR_ARG;
+  const size_t smem = (size_t)((Op::kDot ? m : 0) + (Op::kAxpy ? m : 0)) * 8;
+  if (smem > 220 * 1024) return SKB_ERR_UNSUPPORTED;  // m <= 14080 with both vectors
+  const int per_sm = smem <= 100 * 1024 ? 2 : 1;
+  int grid = skb_num_sms() * per_sm;
+  const int64_t need = (n + kCscThreads - 1) / kCscThreads;
+  if (need < grid) grid = (int)std::max<int64_t>(1, need);
+  double* part = nullptr;
+  if (Op::kAxpy) {
+    part = (double*)skb_ws_take(ws, (size_t)grid * m * 8);
+    if (!part) return SKB_ERR_WORKSPACE;
+  }
+  auto kern = csc_kernel<Op>;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return SKB_ERR_CUDA;
+    configured = smem;
+  }
+  if (n > 0)
+    kern<<<grid, kCscThreads, smem, st>>>(colptr, rowidx, vals, m, n, z, part, op, gate);
+  if (Op::kAxpy)
+    reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, n > 0 ? grid : 0, m, sub, out,
+                                                          gate);
+  return skb_launch_status(__func__);
+}
+
+}  // namespace skb
+
+namespace skb {
+__global__ void csc_to_dense_kernel(const int64_t* __restrict__ colptr,
+                                    const int32_t* __restrict__ rowidx,
+                                    const double* __restrict__ vals, int64_t n, double* A,
+                                    int64_t lda) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  for (int64_t e = colptr[j]; e < colptr[j + 1]; ++e) A[j * lda + rowidx[e]] = vals[e];
+}
+}  // namespace skb
+
+// Dense column-major copy of a CSC matrix (A pre-zeroed, lda >= m): lets the
+// dense-only paths (direct solver, phase 1) run on sparse inputs.
+extern "C" int skb_csc_to_dense(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                                int64_t n, double* A, int64_t lda, void* stream) {
+  if (n <= 0) return 0;
+  csc_to_dense_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      colptr, rowidx, vals, n, A, lda);
+  return skb_launch_status(__func__);
+}
+
+#define SKB_CSC const int64_t *colptr, const int32_t *rowidx, const double *vals, int64_t m, \
+                int64_t n
+
+extern "C" int skb_csc_normal_apply(SKB_CSC, const double* d2, const double* z, double* u,
+                                    const double* sub, const int* gate, void* workspace,
+                                    size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpNormal op{d2};
+  return run_csc(colptr, rowidx, vals, (int)m, n, z, u, sub, op, &ws, (cudaStream_t)stream, gate);
+}
+
+extern "C" int skb_csc_gemv(SKB_CSC, const double* x, double* u, const double* sub,
+                            void* workspace, size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpGemvX op{x};
+  return run_csc(colptr, rowidx, vals, (int)m, n, nullptr, u, sub, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_csc_gemv_ratio(SKB_CSC, const double* v, const double* s, double* u,
+                                  const double* sub, void* workspace, size_t ws_bytes,
+                                  void* stream) {
+  SKB_WS;
+  OpGemvRatio op{v, s};
+  return run_csc(colptr, rowidx, vals, (int)m, n, nullptr, u, sub, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_csc_rhs(SKB_CSC, const double* x, const double* s, const double* r_d,
+                           double sigma_mu, double* p, const double* r_p, void* workspace,
+                           size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpRhs op{x, s, r_d, sigma_mu};
+  return run_csc(colptr, rowidx, vals, (int)m, n, nullptr, p, r_p, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_csc_gemv_t(SKB_CSC, const double* y, const double* add, const double* sub,
+                              double* t, void* workspace, size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpGemvT op{add, sub, t};
+  return run_csc(colptr, rowidx, vals, (int)m, n, y, nullptr, nullptr, op, &ws,
+                 (cudaStream_t)stream);
+}
+
+extern "C" int skb_csc_directions(SKB_CSC, const double* dy, const double* x, const double* s,
+                                  const double* v, const double* r_d, double sigma_mu, double* ds,
+                                  double* dx, double* atdy, double* adx, void* workspace,
+                                  size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpDir op{x, s, v, r_d, sigma_mu, ds, dx, atdy};
+  return run_csc(colptr, rowidx, vals, (int)m, n, dy, adx, nullptr, op, &ws,
+                 (cudaStream_t)stream);
+}
+
+extern "C" int skb_csc_iterate(SKB_CSC, const double* x, const double* dx, const double* s,
+                               const double* ds, double alpha, const double* y_new,
+                               const double* b, const double* c, double* x_out, double* s_out,
+                               double* r_p, double* r_d, void* workspace, size_t ws_bytes,
+                               void* stream) {
+  SKB_WS;
+  OpIter op{x, dx, s, ds, c, alpha, x_out, s_out, r_d};
+  return run_csc(colptr, rowidx, vals, (int)m, n, y_new, r_p, b, op, &ws, (cudaStream_t)stream);
+}

@@ -72,58 +72,106 @@ def _p(t):
     return None if t is None else t
 
 
-def normal_apply(A: DeviceMatrix, d2, z, out, sub=None):
+class SparseDeviceMatrix:
+    """Sparse A (m x n) stored as CSC on the device (config c4): colptr int64
+    (n+1), rowidx int32, vals float64. Column slices share the arrays."""
+
+    is_sparse = True
+
+    def __init__(self, colptr: torch.Tensor, rowidx: torch.Tensor, vals: torch.Tensor, m: int):
+        self.colptr, self.rowidx, self.vals = colptr, rowidx, vals
+        self.m = int(m)
+        self.n = int(colptr.numel() - 1)
+        self.lda = None
+
+    @property
+    def shape(self):
+        return (self.m, self.n)
+
+    @classmethod
+    def from_host(cls, A, device=None) -> "SparseDeviceMatrix":
+        import scipy.sparse as sp
+        device = device or require_cuda()
+        csc = sp.csc_matrix(A, dtype=np.float64)
+        csc.sort_indices()
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)  # noqa
+        return cls(t(csc.indptr, np.int64), t(csc.indices, np.int32), t(csc.data, np.float64),
+                   csc.shape[0])
+
+    def args(self):
+        return (self.colptr, self.rowidx, self.vals, self.m, self.n)
+
+    def to_dense(self) -> "DeviceMatrix":
+        """Dense column-major copy on the device (for the dense-only paths)."""
+        cols = torch.zeros((self.n, lda_for(self.m)), dtype=F64, device=self.vals.device)
+        _lib.call("skb_csc_to_dense", self.colptr, self.rowidx, self.vals, self.n, cols,
+                  cols.shape[1], stream_ptr())
+        return DeviceMatrix(cols, self.m)
+
+
+def _amat(A):
+    """-> (C symbol prefix, leading C arguments) for a dense or CSC matrix."""
+    if getattr(A, "is_sparse", False):
+        return "skb_csc_", A.args()
+    return "skb_", (A.cols, A.m, A.n, A.lda)
+
+
+def normal_apply(A, d2, z, out, sub=None, gate=None):
     """out = A (d2 .* (A' z)) [- sub]   (krylov_solvers.py:46-47)."""
     ws, cap = _ws(A.m)
-    _lib.call("skb_normal_apply", A.cols, A.m, A.n, A.lda, d2, z, out, _p(sub), None, ws, cap,
-              stream_ptr())
+    pre, args = _amat(A)
+    _lib.call(pre + "normal_apply", *args, d2, z, out, _p(sub), gate, ws, cap, stream_ptr())
     return out
 
 
-def gemv(A: DeviceMatrix, x, out, sub=None):
+def gemv(A, x, out, sub=None):
     """out = A x [- sub]   (lp.A @ x, ipm_core.py:99)."""
     ws, cap = _ws(A.m)
-    _lib.call("skb_gemv", A.cols, A.m, A.n, A.lda, x, out, _p(sub), ws, cap, stream_ptr())
+    pre, args = _amat(A)
+    _lib.call(pre + "gemv", *args, x, out, _p(sub), ws, cap, stream_ptr())
     return out
 
 
-def gemv_ratio(A: DeviceMatrix, v, s, out, sub=None):
+def gemv_ratio(A, v, s, out, sub=None):
     """out = A (v / s) [- sub]   (ipm_core.py:502)."""
     ws, cap = _ws(A.m)
-    _lib.call("skb_gemv_ratio", A.cols, A.m, A.n, A.lda, v, s, out, _p(sub), ws, cap,
-              stream_ptr())
+    pre, args = _amat(A)
+    _lib.call(pre + "gemv_ratio", *args, v, s, out, _p(sub), ws, cap, stream_ptr())
     return out
 
 
-def rhs(A: DeviceMatrix, x, s, sigma_mu: float, out, r_d=None, r_p=None):
+def rhs(A, x, s, sigma_mu: float, out, r_d=None, r_p=None):
     """build_rhs (ipm_core.py:196-206)."""
     ws, cap = _ws(A.m)
-    _lib.call("skb_rhs", A.cols, A.m, A.n, A.lda, x, s, _p(r_d), float(sigma_mu), out, _p(r_p),
-              ws, cap, stream_ptr())
-    return out
-
-
-def gemv_t(A: DeviceMatrix, y, out, add=None, sub=None):
-    """out = (A' y [+ add]) [- sub]   (ipm_core.py:100,218)."""
-    ws, cap = _ws(A.m)
-    _lib.call("skb_gemv_t", A.cols, A.m, A.n, A.lda, y, _p(add), _p(sub), out, ws, cap,
+    pre, args = _amat(A)
+    _lib.call(pre + "rhs", *args, x, s, _p(r_d), float(sigma_mu), out, _p(r_p), ws, cap,
               stream_ptr())
     return out
 
 
-def directions(A: DeviceMatrix, dy, x, s, v, sigma_mu, ds, dx, adx, atdy=None, r_d=None):
+def gemv_t(A, y, out, add=None, sub=None):
+    """out = (A' y [+ add]) [- sub]   (ipm_core.py:100,218)."""
+    ws, cap = _ws(A.m)
+    pre, args = _amat(A)
+    _lib.call(pre + "gemv_t", *args, y, _p(add), _p(sub), out, ws, cap, stream_ptr())
+    return out
+
+
+def directions(A, dy, x, s, v, sigma_mu, ds, dx, adx, atdy=None, r_d=None):
     """assemble_directions' A-passes in one sweep (ipm_core.py:218-223)."""
     ws, cap = _ws(A.m)
-    _lib.call("skb_directions", A.cols, A.m, A.n, A.lda, dy, x, s, v, _p(r_d), float(sigma_mu),
-              ds, dx, _p(atdy), adx, ws, cap, stream_ptr())
+    pre, args = _amat(A)
+    _lib.call(pre + "directions", *args, dy, x, s, v, _p(r_d), float(sigma_mu), ds, dx, _p(atdy),
+              adx, ws, cap, stream_ptr())
 
 
-def iterate(A: DeviceMatrix, x, s, y_new, b, c, r_p, r_d, dx=None, ds=None, alpha=0.0,
-            x_out=None, s_out=None):
+def iterate(A, x, s, y_new, b, c, r_p, r_d, dx=None, ds=None, alpha=0.0, x_out=None,
+            s_out=None):
     """make_iterate's A-passes in one sweep (ipm_core.py:94-102)."""
     ws, cap = _ws(A.m)
-    _lib.call("skb_iterate", A.cols, A.m, A.n, A.lda, x, _p(dx), s, _p(ds), float(alpha), y_new,
-              b, c, _p(x_out), _p(s_out), r_p, r_d, ws, cap, stream_ptr())
+    pre, args = _amat(A)
+    _lib.call(pre + "iterate", *args, x, _p(dx), s, _p(ds), float(alpha), y_new, b, c,
+              _p(x_out), _p(s_out), r_p, r_d, ws, cap, stream_ptr())
 
 
 def sparse_embedding(key0: int, key1: int, n: int, w: int, s: int, device=None):

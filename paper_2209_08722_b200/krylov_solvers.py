@@ -107,7 +107,7 @@ def pcg(op, f: PreconditionerFactor, p: torch.Tensor, t_max: int, tol: float):
     B = _buffers(m, t_max, dev)
     dy = torch.empty(m, dtype=F64, device=dev)
     lp = getattr(op, "lp", None)
-    if isinstance(op, NormalOperator) and not lp.comm.active:
+    if isinstance(op, NormalOperator) and not lp.comm.active and not lp.sparse:
         ws, cap = workspace(int(_lib.lib().skb_stream_workspace_bytes(m)))
         _lib.call("skb_pcg_solve", lp.A.cols, m, lp.A.n, lp.A.lda, op._d2, f.Linv, f.LinvT, f.ld,
                   p, dy, B.vec, B.ldv, t_max, float(tol), B.state, B.trace,
@@ -257,8 +257,8 @@ def direct_solve(op: "NormalOperator", p: torch.Tensor, cap: int = DIRECT_CAP) -
     dev = p.device
     G = torch.zeros((Mp, Mp), dtype=F64, device=dev)
     ws, cap_b = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, m)))
-    _lib.call("skb_weighted_gram", lp.A.cols, m, lp.A.n, lp.A.lda, op._d2, G, Mp, ws, cap_b,
-              stream_ptr())
+    Ad = lp.dense_A()
+    _lib.call("skb_weighted_gram", Ad.cols, m, Ad.n, Ad.lda, op._d2, G, Mp, ws, cap_b, stream_ptr())
     if lp.comm.active:
         lp.comm.allreduce_(G)
     _lib.call("skb_set_identity_pad", G, Mp, m, Mp, stream_ptr())

@@ -25,6 +25,9 @@ from .errors import DimensionMismatch, ZeroRow
 from .runtime import F64, require_cuda, stream_ptr, workspace
 
 
+SPARSE_DENSITY = 0.1  # CSC device storage below this fill (12 B/nnz vs 8 B/entry dense)
+
+
 @dataclass
 class LinearProgram:
     """min c'x s.t. Ax = b, x >= 0; A is scipy CSR or a dense numpy array."""
@@ -100,7 +103,18 @@ class DeviceLP:
         st = self.vec_stats(self.b, global_=False)
         self.b_norm = math.sqrt(st[0])
         self.c_norm = math.sqrt(self.vec_stats(self.c)[0])
-        self.a_scale = math.sqrt(self.vec_stats(A.cols.view(-1))[0])
+        self.sparse = bool(getattr(A, "is_sparse", False))
+        self.a_scale = math.sqrt(self.vec_stats(A.vals if self.sparse else A.cols.view(-1))[0])
+        self._dense = None
+
+    def dense_A(self) -> "K.DeviceMatrix":
+        """A in the dense column-major layout (a device-side copy for CSC inputs,
+        used by the dense-only paths: direct solver, phase 1, Gaussian GEMM)."""
+        if not self.sparse:
+            return self.A
+        if self._dense is None:
+            self._dense = self.A.to_dense()
+        return self._dense
 
     # ---------------------------------------------------------- construction
     @classmethod
@@ -113,9 +127,13 @@ class DeviceLP:
         j0, j1 = comm.shard(n)
         if sp.issparse(A):
             blk = A.tocsc()[:, j0:j1]
+            # genuinely sparse inputs stay CSC on the device (config c4); dense data that
+            # arrives as CSR (make_lp always stores CSR) is streamed column-major
+            density = blk.nnz / max(1, blk.shape[0] * blk.shape[1])
+            Ad = (K.SparseDeviceMatrix.from_host(blk, device) if density < SPARSE_DENSITY
+                  else K.DeviceMatrix.from_host(blk, device))
         else:
-            blk = np.asarray(A)[:, j0:j1]
-        Ad = K.DeviceMatrix.from_host(blk, device)
+            Ad = K.DeviceMatrix.from_host(np.asarray(A)[:, j0:j1], device)
         return cls(Ad, _dev(lp.b, device), _dev(np.asarray(lp.c)[j0:j1], device), n, j0, comm,
                    getattr(lp, "name", "lp"))
 
@@ -162,9 +180,7 @@ class DeviceLP:
 
     def normal(self, d2, z, out=None, sub=None, gate=None):
         out = self.new_m() if out is None else out
-        ws, cap = K._ws(self.m)
-        _lib.call("skb_normal_apply", self.A.cols, self.m, self.A.n, self.A.lda, d2, z, out,
-                  self._sub_arg(sub), gate, ws, cap, stream_ptr())
+        K.normal_apply(self.A, d2, z, out, sub=self._sub_arg(sub), gate=gate)
         return self._finish_m(out, sub)
 
     def rhs(self, x, s, sigma_mu, r_d=None, r_p=None, out=None):

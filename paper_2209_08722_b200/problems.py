@@ -63,6 +63,57 @@ def wide_dense_lp(m: int, n: int, seed: int = 0) -> DenseLP:
     return DenseLP(A, b, c, x0, y0, s0, name=f"wide_dense_{m}x{n}_s{seed}")
 
 
+@dataclass
+class SparseLP:
+    """Config c4: A (m x n, scipy CSC) with k nonzeros per column, feasible start."""
+
+    A: object
+    b: np.ndarray
+    c: np.ndarray
+    x0: np.ndarray
+    y0: np.ndarray
+    s0: np.ndarray
+    name: str = "sparse_lp"
+
+    @property
+    def m(self) -> int:
+        return self.A.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.A.shape[1]
+
+    def theta0(self) -> float:
+        return float(np.min(self.x0 * self.s0) / (float(self.x0 @ self.s0) / self.n))
+
+    def gamma_run(self, gamma: float) -> float:
+        return max(gamma, 1.0 - 0.999 * self.theta0())
+
+
+def sparse_wide_lp(m: int, n: int, k: int = 5, seed: int = 0) -> SparseLP:
+    """config c4: per column k distinct rows from
+    G.integers(0, m, (n, k)) with duplicate rows redrawn, values
+    G.standard_normal((n, k)), then y0, x0, s0 as for the dense configs."""
+    import scipy.sparse as sp
+    g = np.random.Generator(np.random.Philox(int(seed)))
+    rows = g.integers(0, m, size=(n, k))
+    while True:
+        dup = (np.diff(np.sort(rows, axis=1), axis=1) == 0).any(axis=1)
+        if not dup.any():
+            break
+        rows[dup] = g.integers(0, m, size=(int(dup.sum()), k))
+    vals = g.standard_normal((n, k))
+    y0 = g.standard_normal(m)
+    x0 = g.uniform(0.5, 1.5, n)
+    s0 = g.uniform(0.5, 1.5, n)
+    colptr = np.arange(0, n * k + 1, k, dtype=np.int64)
+    A = sp.csc_matrix((vals.ravel(), rows.ravel(), colptr), shape=(m, n))
+    A.sort_indices()
+    b = A @ x0
+    c = A.T @ y0 + s0
+    return SparseLP(A, b, c, x0, y0, s0, name=f"sparse_wide_{m}x{n}_k{k}_s{seed}")
+
+
 def random_feasible_dense(m: int, n: int, density: float, seed: int):
     """The reference's random_feasible_lp instance (lp_model.py:134-160), same
     draw order: mask, values, diagonal boost, x_feas, y0, slack. Returns dense

@@ -144,21 +144,27 @@ def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = 
     ldx = lda_for(m)
     X = torch.empty((W.w, ldx), dtype=F64, device=d.device)
     if W.kind == "identity":
+        Ad = lp.dense_A()
         if lp.comm.active:
             X.zero_()
             sub = X[lp.j0:lp.j0 + A.n]
-            _lib.call("skb_scale_columns", A.cols, m, A.n, A.lda, d, sub, ldx, stream_ptr())
+            _lib.call("skb_scale_columns", Ad.cols, m, Ad.n, Ad.lda, d, sub, ldx, stream_ptr())
         else:
-            _lib.call("skb_scale_columns", A.cols, m, A.n, A.lda, d, X, ldx, stream_ptr())
+            _lib.call("skb_scale_columns", Ad.cols, m, Ad.n, Ad.lda, d, X, ldx, stream_ptr())
     elif W.kind == "sparse_sign":
         need = int(_lib.lib().skb_sketch_workspace_bytes(A.n, W.w, W.s))
         ws, cap = workspace(need)
-        _lib.call("skb_sketch_apply", A.cols, m, A.n, A.lda, d, W.cols, W.vals, W.s, W.w, X, ldx,
-                  ws, cap, stream_ptr())
+        if lp.sparse:  # CSC A (config c4)
+            _lib.call("skb_csc_sketch_apply", *A.args(), d, W.cols, W.vals, W.s, W.w, X, ldx, ws,
+                      cap, stream_ptr())
+        else:
+            _lib.call("skb_sketch_apply", A.cols, m, A.n, A.lda, d, W.cols, W.vals, W.s, W.w, X,
+                      ldx, ws, cap, stream_ptr())
     else:  # dense Gaussian: one DMMA GEMM, X = W' D A' (sketching.py:158-159)
+        Ad = lp.dense_A()
         ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, W.w)))
-        _lib.call("skb_gaussian_apply", A.cols, m, A.n, A.lda, d, W.dense, W.w, X, ldx, ws, cap,
-                  stream_ptr())
+        _lib.call("skb_gaussian_apply", Ad.cols, m, Ad.n, Ad.lda, d, W.dense, W.w, X, ldx, ws,
+                  cap, stream_ptr())
     if ldx != m:
         X[:, m:].zero_()
     if lp.comm.active:

@@ -50,7 +50,7 @@ def phase1_lp(lp: DeviceLP):
         raise NotImplementedError("phase 1 on a column-sharded LP")
     lda = lp.A.lda
     cols = torch.zeros((n + m, lda), dtype=F64, device=lp.device)
-    cols[:n, :m].copy_(lp.A.cols[:, :m] * sign[None, :])          # A_f = diag(sign) A
+    cols[:n, :m].copy_(lp.dense_A().cols[:, :m] * sign[None, :])  # A_f = diag(sign) A
     cols[n + torch.arange(m, device=lp.device), torch.arange(m, device=lp.device)] = 1.0
     Aaux = DeviceMatrix(cols, m)
     c_aux = torch.cat([torch.zeros(n, dtype=F64, device=lp.device),
@@ -80,8 +80,8 @@ def _chol_solve_aat(lp: DeviceLP, rhs: torch.Tensor) -> torch.Tensor:
     G = torch.zeros((Mp, Mp), dtype=F64, device=lp.device)
     ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, m)))
     ones = torch.ones(lp.n_local, dtype=F64, device=lp.device)
-    _lib.call("skb_weighted_gram", lp.A.cols, m, lp.A.n, lp.A.lda, ones, G, Mp, ws, cap,
-              stream_ptr())
+    Ad = lp.dense_A()
+    _lib.call("skb_weighted_gram", Ad.cols, m, Ad.n, Ad.lda, ones, G, Mp, ws, cap, stream_ptr())
     lp.comm.allreduce_(G)
     _lib.call("skb_set_identity_pad", G, Mp, m, Mp, stream_ptr())
     status = torch.zeros(1, dtype=torch.int32, device=lp.device)
@@ -109,7 +109,8 @@ def phase1_point(lp: DeviceLP, params):
     if z_sum > 1e-7 * (1.0 + lp.b_norm):
         raise Infeasible(f"phase-1 optimum 1'z = {z_sum:.3e} is bounded away from zero")
     x0 = torch.from_numpy(np.ascontiguousarray(rep.x[:lp.n])).to(lp.device)
-    _lib.call("skb_zero_col_fill", lp.A.cols, lp.m, lp.A.n, lp.A.lda, x0, stream_ptr())
+    Ad = lp.dense_A()
+    _lib.call("skb_zero_col_fill", Ad.cols, lp.m, Ad.n, Ad.lda, x0, stream_ptr())
     try:
         resid = lp.gemv(x0, sub=lp.b)                 # A x0 - b
         resid.neg_()                                  # b - A x0

@@ -201,6 +201,31 @@ def gaussian_traces():
         json.dump(res, f)
 
 
+def sparse_traces():
+    """Config c4's generator at reduced size (5 nnz per column), s = 4 and s = 1."""
+    from paper_2209_08722_b200.problems import sparse_wide_lp
+    res = {}
+    lpd = sparse_wide_lp(100, 20_000, 5, 7)
+    lp = skipm.make_lp(lpd.A, lpd.b, lpd.c, name=lpd.name)
+    for s_nnz in (4, 1):
+        start = ipm_core.make_iterate(lp, lpd.x0, lpd.y0, lpd.s0)
+        prm = ipm_core.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5, w=400,
+                                 s=s_nnz, tol_outer=1e-6, seed=11)
+        rep = ipm_core.solve(lp, start, prm)
+        d = rep.to_dict()
+        d.pop("params")
+        res[f"s{s_nnz}"] = d
+        print(f"sparse s={s_nnz}: outer {rep.outer} inner {rep.sum_inner} obj {rep.objective!r}")
+    # ADW bits for the CSC sketch kernel
+    W = sketching.build_sparse_embedding(lpd.n, 400, 4, 77)
+    g = np.random.Generator(np.random.Philox(78))
+    d = 10.0 ** g.uniform(-3, 3, lpd.n)
+    adw = sketching.apply_sketch(lp.A, d, W)
+    res["adw_sha256"] = sha(adw)
+    with open(os.path.join(HERE, "sparse_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
 def start_traces():
     """solve() with no start in feasible mode: phase 1 + shifted dual + centering
     (ipm_core.py:814-969) on the reference's random_feasible_lp instance."""
@@ -226,7 +251,10 @@ def start_traces():
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers", "start", "gaussian"]
+    what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers", "start", "gaussian",
+                            "sparse"]
+    if "sparse" in what:
+        sparse_traces()
     if "gaussian" in what:
         gaussian_traces()
     if "start" in what:

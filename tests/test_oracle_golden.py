@@ -148,6 +148,23 @@ def test_config1_trace(s_nnz):
     _compare_solve(O.solve(A, lpd.b, lpd.c, st, prm), gold[f"s{s_nnz}"], 1e-12)
 
 
+def test_sparse_config_trace_and_adw():
+    from paper_2209_08722_b200.problems import sparse_wide_lp
+    with open(os.path.join(GOLDEN, "sparse_traces.json")) as f:
+        gold = json.load(f)
+    lpd = sparse_wide_lp(100, 20_000, 5, 7)
+    A = sp.csr_matrix(lpd.A)
+    A.sort_indices()
+    st = O.make_iterate(A, lpd.b, lpd.c, lpd.x0, lpd.y0, lpd.s0)
+    prm = O.Params(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5, w=400, s=4,
+                   tol_outer=1e-6, seed=11)
+    _compare_solve(O.solve(A, lpd.b, lpd.c, st, prm), gold["s4"], 1e-12)
+    cols, vals = O.sparse_embedding(lpd.n, 400, 4, 77)
+    d = 10.0 ** np.random.Generator(np.random.Philox(78)).uniform(-3, 3, lpd.n)
+    W = O.Sketch("sparse_sign", lpd.n, 400, 4, 77, cols=cols, vals=vals)
+    assert _sha(O.apply_sketch(A, d, W)) == gold["adw_sha256"]
+
+
 def test_gaussian_sketch_and_traces():
     from paper_2209_08722_b200.problems import ill_conditioned_lp
     with open(os.path.join(GOLDEN, "gaussian_traces.json")) as f:
