@@ -175,6 +175,199 @@ __global__ void __launch_bounds__(128) dgemm_kernel(GemmArgs g) {
       }
 }
 
+// Pipelined variant for 16-byte-aligned operands (even leading dims and batch
+// strides, 16 B base pointers): CTA tile 128 x 64 x 16, 8 warps (4 x 2) of
+// 32 x 32, a 3-stage cp.async ring (zero-filled at the M/N/K edges) so the
+// global loads never pass through registers. Shared tiles keep the global
+// orientation with row strides = 4 (mod 16) doubles, which makes every
+// fragment read conflict-free in both 16-lane phases. Same k order and the
+// same products as dgemm_kernel (kscale is applied to the A fragment).
+constexpr int PBM = 128, PBN = 64, PBK = 16, PST = 3;
+
+template <int TA>
+struct PTileA {  // TA=1: [k][i] (16 x 128), TA=0: [i][k] (128 x 16)
+  static constexpr int kStride = TA ? PBM + 4 : PBK + 4;
+  static constexpr int kSize = TA ? PBK * kStride : PBM * kStride;
+};
+template <int TB>
+struct PTileB {  // TB=0: [k][j] (16 x 64), TB=1: [j][k] (64 x 16)
+  static constexpr int kStride = TB ? PBK + 4 : PBN + 4;
+  static constexpr int kSize = TB ? PBN * kStride : PBK * kStride;
+};
+
+SKB_DEV void cp_async16(double* smem, const double* gmem, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+SKB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+SKB_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int TA, int TB>
+__global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmArgs g) {
+  extern __shared__ __align__(16) double psm[];
+  using TAt = PTileA<TA>;
+  using TBt = PTileB<TB>;
+  constexpr int kStage = TAt::kSize + TBt::kSize;
+  const int batch = blockIdx.z / g.splits, split = blockIdx.z % g.splits;
+  const int bm = blockIdx.y, bn = blockIdx.x;
+  if (g.lower_only && bn * PBN > bm * PBM + PBM - 1) return;
+  const int i0 = bm * PBM, j0 = bn * PBN;
+  const double* A = g.A + (int64_t)batch * g.sA;
+  const double* B = g.B + (int64_t)batch * g.sB;
+  const int k_begin = split * g.kchunk, k_end = min(g.K, k_begin + g.kchunk);
+  const int nk = k_end > k_begin ? (k_end - k_begin + PBK - 1) / PBK : 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  auto load_stage = [&](int t, int stage) {
+    double* As = psm + stage * kStage;
+    double* Bs = As + TAt::kSize;
+    const int k0 = k_begin + t * PBK;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {  // A: 1024 16-byte chunks
+      const int c = tid + 256 * e;
+      int kk, ii, bytes;
+      const double* src;
+      double* dst;
+      if (TA) {
+        kk = c >> 6;
+        ii = (c & 63) * 2;
+        const int gi = i0 + ii, gk = k0 + kk;
+        bytes = gk < k_end ? max(0, min(16, (g.M - gi) * 8)) : 0;
+        src = bytes ? A + (int64_t)gk * g.lda + gi : A;
+        dst = As + kk * TAt::kStride + ii;
+      } else {
+        ii = c >> 3;
+        kk = (c & 7) * 2;
+        const int gi = i0 + ii, gk = k0 + kk;
+        bytes = gi < g.M ? max(0, min(16, (k_end - gk) * 8)) : 0;
+        src = bytes ? A + (int64_t)gi * g.lda + gk : A;
+        dst = As + ii * TAt::kStride + kk;
+      }
+      cp_async16(dst, src, bytes);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {  // B: 512 chunks
+      const int c = tid + 256 * e;
+      int kk, jj, bytes;
+      const double* src;
+      double* dst;
+      if (TB) {
+        jj = c >> 3;
+        kk = (c & 7) * 2;
+        const int gj = j0 + jj, gk = k0 + kk;
+        bytes = gj < g.N ? max(0, min(16, (k_end - gk) * 8)) : 0;
+        src = bytes ? B + (int64_t)gj * g.ldb + gk : B;
+        dst = Bs + jj * TBt::kStride + kk;
+      } else {
+        kk = c >> 5;
+        jj = (c & 31) * 2;
+        const int gj = j0 + jj, gk = k0 + kk;
+        bytes = gk < k_end ? max(0, min(16, (g.N - gj) * 8)) : 0;
+        src = bytes ? B + (int64_t)gk * g.ldb + gj : B;
+        dst = Bs + kk * TBt::kStride + jj;
+      }
+      cp_async16(dst, src, bytes);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < PST - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int t = 0; t < nk; ++t) {
+    cp_async_wait<PST - 2>();
+    __syncthreads();
+    if (t + PST - 1 < nk) load_stage(t + PST - 1, (t + PST - 1) % PST);
+    cp_async_commit();
+    const double* As = psm + (t % PST) * kStage;
+    const double* Bs = As + TAt::kSize;
+    const int k0 = k_begin + t * PBK;
+#pragma unroll
+    for (int kk = 0; kk < PBK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        af[a] = TA ? As[(kk + tq) * TAt::kStride + wm + a * 8 + gq]
+                   : As[(wm + a * 8 + gq) * TAt::kStride + kk + tq];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        bf[b] = TB ? Bs[(wn + b * 8 + gq) * TBt::kStride + kk + tq]
+                   : Bs[(kk + tq) * TBt::kStride + wn + b * 8 + gq];
+      if (g.kscale) {
+        const int gk = k0 + kk + tq;
+        const double sc = gk < k_end ? g.kscale[gk] : 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) af[a] *= sc;
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(acc[a][b], af[a], bf[b]);
+    }
+  }
+  cp_async_wait<0>();
+
+  const bool direct = g.splits == 1;
+  double* C = direct ? g.C + (int64_t)batch * g.sC
+                     : g.part + ((int64_t)blockIdx.z) * (int64_t)g.M * g.N;
+  const int64_t ldc = direct ? g.ldc : g.N;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = i0 + wm + a * 8 + gq, j = j0 + wn + b * 8 + tq * 2 + q;
+        if (i < g.M && j < g.N) {
+          double* dst = C + (int64_t)i * ldc + j;
+          if (direct) {
+            double v = g.alpha * acc[a][b][q];
+            if (g.beta != 0.0) v = fma(g.beta, *dst, v);
+            *dst = v;
+          } else {
+            *dst = acc[a][b][q];
+          }
+        }
+      }
+}
+
+template <int TA, int TB>
+static size_t pipe_smem_bytes() {
+  return (size_t)PST * (PTileA<TA>::kSize + PTileB<TB>::kSize) * sizeof(double);
+}
+
+template <int TA, int TB>
+static void launch_pipe(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  static bool configured = false;  // one per template instantiation
+  const size_t smem = pipe_smem_bytes<TA, TB>();
+  if (!configured) {
+    cudaFuncSetAttribute(dgemm_pipe_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = true;
+  }
+  dgemm_pipe_kernel<TA, TB><<<grid, 256, smem, st>>>(g);
+}
+
+static bool pipe_ok(const GemmArgs& g) {
+  if (getenv("SKB_GEMM_NOPIPE")) return false;
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  return al(g.A) && al(g.B) && (g.lda % 2 == 0) && (g.ldb % 2 == 0) && (g.sA % 2 == 0) &&
+         (g.sB % 2 == 0);
+}
+
 __global__ void gemm_splitk_reduce_kernel(GemmArgs g, int nbatch) {
   const int64_t MN = (int64_t)g.M * g.N;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -473,7 +666,9 @@ using namespace skb;
 static int gemm_launch(const GemmArgs& base, int nbatch, skb_ws* ws, cudaStream_t st) {
   GemmArgs g = base;
   if (g.M <= 0 || g.N <= 0) return 0;
-  const int tm = (g.M + GBM - 1) / GBM, tn = (g.N + GBN - 1) / GBN;
+  const bool pipe = pipe_ok(g);
+  const int bmt = pipe ? PBM : GBM, bnt = pipe ? PBN : GBN;
+  const int tm = (g.M + bmt - 1) / bmt, tn = (g.N + bnt - 1) / bnt;
   int tiles = tm * tn * nbatch;
   if (g.lower_only) tiles = (tiles + 1) / 2;
   const int target = 2 * skb_num_sms();
@@ -501,7 +696,16 @@ static int gemm_launch(const GemmArgs& base, int nbatch, skb_ws* ws, cudaStream_
   }
   if (g.K <= 0) g.kchunk = 1;
   dim3 grid(tn, tm, nbatch * g.splits);
-  dgemm_kernel<<<grid, 128, 0, st>>>(g);
+  if (!pipe)
+    dgemm_kernel<<<grid, 128, 0, st>>>(g);
+  else if (g.ta && g.tb)
+    launch_pipe<1, 1>(g, grid, st);
+  else if (g.ta)
+    launch_pipe<1, 0>(g, grid, st);
+  else if (g.tb)
+    launch_pipe<0, 1>(g, grid, st);
+  else
+    launch_pipe<0, 0>(g, grid, st);
   if (g.splits > 1) {
     const int64_t tot = (int64_t)g.M * g.N * nbatch;
     gemm_splitk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g, nbatch);

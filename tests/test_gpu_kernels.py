@@ -182,3 +182,50 @@ def test_rhs_directions_iterate(K, mode):
     ref_rp, ref_rd = A @ xn - b, A.T @ ynew + sn - c
     assert np.max(np.abs(_h(rp) - ref_rp)) <= 1e-13 * (np.abs(A) @ np.abs(xn)).max()
     assert np.max(np.abs(_h(rd) - ref_rd)) <= 1e-13 * (np.abs(A.T) @ np.abs(ynew) + 1).max()
+
+
+# ------------------------------------------------------------ DMMA GEMM
+GEMM_CASES = [(129, 65, 37, 0), (300, 200, 1000, 0), (1000, 1000, 4000, 1), (64, 64, 16, 0),
+              (257, 130, 3, 0), (1024, 512, 2048, 1)]
+
+
+@pytest.mark.parametrize("M,N,Kd,lower", GEMM_CASES)
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("pipe", [True, False])
+def test_gemm_against_numpy(K, monkeypatch, M, N, Kd, lower, ta, tb, pipe):
+    """skb_gemm (both the cp.async 128x64 kernel and the register-staged
+    fallback) against numpy fp64; error bound 1e-13 * sum|a||b|."""
+    from paper_2209_08722_b200 import _lib
+    from paper_2209_08722_b200.runtime import stream_ptr, workspace
+    if not pipe:
+        monkeypatch.setenv("SKB_GEMM_NOPIPE", "1")
+    g = np.random.Generator(np.random.Philox(M * 7 + N + Kd))
+    opa = g.standard_normal((M, Kd))
+    opb = g.standard_normal((Kd, N))
+    A = opa.T.copy() if ta else opa.copy()
+    B = opb.T.copy() if tb else opb.copy()
+    C0 = g.standard_normal((M, N))
+    Cd = _t(C0)
+    ws, cap = workspace(1 << 26)
+    _lib.call("skb_gemm", ta, tb, M, N, Kd, 0.5, _t(A), A.shape[1], _t(B), B.shape[1], -1.0, Cd, N,
+              lower, 1, 0, 0, 0, ws, cap, stream_ptr())
+    ref = 0.5 * opa @ opb - C0
+    bound = 1e-13 * (np.abs(opa) @ np.abs(opb) + np.abs(C0))
+    out = _h(Cd)
+    mask = np.tril(np.ones((M, N), bool)) if lower else np.ones((M, N), bool)
+    assert np.all(np.abs(out - ref)[mask] <= bound[mask])
+
+
+def test_weighted_gram(K):
+    from paper_2209_08722_b200 import _lib
+    from paper_2209_08722_b200.runtime import stream_ptr, workspace
+    g = np.random.Generator(np.random.Philox(12))
+    m, n = 300, 5000
+    A = g.standard_normal((m, n))
+    wts = g.random(n) + 0.1
+    G = torch.zeros((m, m), dtype=torch.float64, device="cuda")
+    ws, cap = workspace(1 << 26)
+    _lib.call("skb_weighted_gram", _t(A.T), m, n, m, _t(wts), G, m, ws, cap, stream_ptr())
+    ref = (A * wts) @ A.T
+    out = np.tril(_h(G))
+    assert np.max(np.abs(out - np.tril(ref))) <= 1e-12 * np.abs(ref).max()
