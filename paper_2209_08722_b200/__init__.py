@@ -49,6 +49,9 @@ _LAZY = {
     "build_gaussian_sketch": "sketching", "apply_sketch": "sketching",
     "compute_v": "correction", "check_v_norm": "correction",
     "check_v_small_enough": "correction", "CorrectionVector": "correction",
+    "SvmDataset": "ingest", "SvmLpMapping": "ingest", "svm_to_lp": "ingest",
+    "extract_svm_solution": "ingest", "load_libsvm": "ingest", "save_matrix_market": "ingest",
+    "load_matrix_market": "ingest", "to_device": "ingest",
 }
 
 

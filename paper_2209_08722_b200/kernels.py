@@ -101,6 +101,14 @@ class SparseDeviceMatrix:
     def args(self):
         return (self.colptr, self.rowidx, self.vals, self.m, self.n)
 
+    def to_host(self):
+        """scipy CSC copy (column slices rebased to their first entry)."""
+        import scipy.sparse as sp
+        ptr = self.colptr.cpu().numpy()
+        a, b = int(ptr[0]), int(ptr[-1])
+        return sp.csc_matrix((self.vals[a:b].cpu().numpy(), self.rowidx[a:b].cpu().numpy(),
+                              ptr - a), shape=(self.m, self.n))
+
     def to_dense(self) -> "DeviceMatrix":
         """Dense column-major copy on the device (for the dense-only paths)."""
         cols = torch.zeros((self.n, lda_for(self.m)), dtype=F64, device=self.vals.device)

@@ -250,9 +250,64 @@ def start_traces():
         json.dump(res, f)
 
 
+def write_libsvm_sample(path):
+    """A small synthetic LIBSVM file (seeded; comments, blank lines, a repeated
+    index, unsorted indices) for the ingestion parity test."""
+    g = np.random.Generator(np.random.Philox(61))
+    m, n = 30, 12
+    X = np.where(g.random((m, n)) < 0.4, np.round(g.standard_normal((m, n)), 6), 0.0)
+    y = np.sign(X @ g.standard_normal(n) + 1e-3)
+    y[y == 0] = 1.0
+    lines = ["# synthetic sample for tests/test_ingest.py", ""]
+    for i in range(m):
+        idx = [j for j in range(n) if X[i, j] != 0.0]
+        g.shuffle(idx)
+        toks = [f"{j + 1}:{float(X[i, j])!r}" for j in idx]
+        if i == 3 and idx:
+            toks.insert(0, f"{idx[0] + 1}:0.5")   # overwritten by the later token
+        lines.append(f"{int(y[i]):+d} " + " ".join(toks) + ("  # row comment" if i == 5 else ""))
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+def svm_traces():
+    """Ingestion (load_libsvm, svm_to_lp) and the SVM pipeline solves of the
+    reference's acceptance criterion 8 (test_acceptance.py:279-301)."""
+    from skipm import lp_model
+    path = os.path.join(HERE, "svm_small.libsvm")
+    write_libsvm_sample(path)
+    ds = lp_model.load_libsvm(path)
+    lp, mp = lp_model.svm_to_lp(ds)
+    np.savez(os.path.join(HERE, "svm_ingest.npz"), X=ds.X, y=ds.y, A_data=lp.A.data,
+             A_indices=lp.A.indices, A_indptr=lp.A.indptr, b=lp.b, c=lp.c,
+             shape=np.array(lp.A.shape))
+    res = {}
+    g = np.random.Generator(np.random.Philox(42))
+    X50 = g.standard_normal((50, 100))
+    y50 = np.sign(X50 @ g.standard_normal(100))
+    cases = {"two_point": lp_model.SvmDataset(X=np.array([[1.0], [-1.0]]), y=np.array([1.0, -1.0])),
+             "sep50x100": lp_model.SvmDataset(X=X50, y=y50), "libsvm_small": ds}
+    for name, d in cases.items():
+        lpc, mpc = lp_model.svm_to_lp(d)
+        rep = ipm_core.solve(lpc, params=ipm_core.IpmParams(seed=0))
+        w, b = lp_model.extract_svm_solution(mpc, rep.x)
+        dd = rep.to_dict()
+        dd.pop("params")
+        res[name] = dict(outer=rep.outer, objective=rep.objective, converged=rep.converged,
+                         mu_trace=list(map(float, rep.mu_trace)), w=w.tolist(), b=b,
+                         w_l1=float(np.abs(w).sum()),
+                         min_margin=float((d.y * (d.X @ w + b)).min()),
+                         inner_iterations=[r.inner_iterations for r in rep.steps])
+        print(f"svm {name}: outer {rep.outer} obj {rep.objective!r} converged {rep.converged}")
+    with open(os.path.join(HERE, "svm_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers", "start", "gaussian",
-                            "sparse"]
+                            "sparse", "svm"]
+    if "svm" in what:
+        svm_traces()
     if "sparse" in what:
         sparse_traces()
     if "gaussian" in what:
