@@ -58,7 +58,8 @@ int skb_lemire_draw(uint64_t key0, uint64_t key1, uint64_t word_offset, uint32_t
                     void* workspace, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------- K4/K8 column streams --
- * Every call reads A once. m <= 2048 (dense). Outputs that are m-vectors are
+ * Every call reads A once. m <= 16384 (dense; per-warp TMA ring up to 1024,
+ * CTA-cooperative blocks above). Outputs that are m-vectors are
  * summed over column blocks in a fixed order; `sub` (nullable) is subtracted
  * after the sum. Workspace: skb_stream_workspace_bytes(m). */
 size_t skb_stream_workspace_bytes(int64_t m);
@@ -211,9 +212,8 @@ int skb_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, double alp
              int64_t ldc, int32_t lower_only, int32_t batch, int64_t strideA, int64_t strideB,
              int64_t strideC, void* workspace, size_t ws_bytes, void* stream);
 
-/* Blocked Cholesky (lower, in place) and triangular inverse; Mp % 64 == 0
- * (power of two for skb_trtri). status: device int, SKB_ST_CHOL_FAIL on a
- * nonpositive pivot. */
+/* Blocked Cholesky (lower, in place) and triangular inverse; Mp % 64 == 0.
+ * status: device int, SKB_ST_CHOL_FAIL on a nonpositive pivot. */
 int skb_potrf(double* G, int64_t ld, int32_t Mp, int* status, void* workspace, size_t ws_bytes,
               void* stream);
 int skb_trtri(const double* L, double* Li, int64_t ld, int32_t Mp, void* workspace,

@@ -43,7 +43,19 @@ struct GemmArgs {
   double alpha, beta;
   int ta, tb, lower_only;
   const double* kscale;  // optional: opA(i,k) *= kscale[k] (weighted SYRK A diag(w) A')
+  // Triangular operands (zeros outside are skipped, not multiplied): tri_a 1 =
+  // opA lower (k <= i), 2 = upper (k >= i); tri_b 1 = opB lower (k >= j),
+  // 2 = upper (k <= j). Each tile trims its k range accordingly.
+  int tri_a, tri_b;
 };
+
+// The k range [kb, ke) a (i0, j0, bm x bn) tile needs under the tri flags.
+SKB_DEV void tri_krange(const GemmArgs& g, int i0, int j0, int bm, int bn, int& kb, int& ke) {
+  if (g.tri_a == 1) ke = min(ke, i0 + bm);
+  else if (g.tri_a == 2) kb = max(kb, i0);
+  if (g.tri_b == 1) kb = max(kb, j0);
+  else if (g.tri_b == 2) ke = min(ke, j0 + bn);
+}
 
 SKB_DEV void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -60,7 +72,8 @@ __global__ void __launch_bounds__(128) dgemm_kernel(GemmArgs g) {
   const int i0 = bm * GBM, j0 = bn * GBN;
   const double* A = g.A + (int64_t)batch * g.sA;
   const double* B = g.B + (int64_t)batch * g.sB;
-  const int k_begin = split * g.kchunk, k_end = min(g.K, k_begin + g.kchunk);
+  int k_begin = split * g.kchunk, k_end = min(g.K, k_begin + g.kchunk);
+  tri_krange(g, i0, j0, GBM, GBN, k_begin, k_end);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int gq = lane >> 2, tq = lane & 3;
@@ -218,7 +231,8 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmArgs g) {
   const int i0 = bm * PBM, j0 = bn * PBN;
   const double* A = g.A + (int64_t)batch * g.sA;
   const double* B = g.B + (int64_t)batch * g.sB;
-  const int k_begin = split * g.kchunk, k_end = min(g.K, k_begin + g.kchunk);
+  int k_begin = split * g.kchunk, k_end = min(g.K, k_begin + g.kchunk);
+  tri_krange(g, i0, j0, PBM, PBN, k_begin, k_end);
   const int nk = k_end > k_begin ? (k_end - k_begin + PBK - 1) / PBK : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -387,95 +401,106 @@ __global__ void gemm_splitk_reduce_kernel(GemmArgs g, int nbatch) {
 // ----------------------------------------------------------------- Cholesky
 constexpr int NB = 64;
 
-// Unblocked right-looking Cholesky of the 64 x 64 diagonal block at (k0, k0),
-// lower, in place, plus its inverse Dinv = L11^-1 (64 x 64, row-major) which
-// turns the panel TRSM into a GEMM and seeds the triangular inverse.
-// Thread i keeps row i in registers, ROTATED so the current column is always
-// r[0] (static register indices with a runtime step loop: a fully unrolled
-// version thrashed the I-cache, a shared-memory version serialised on
-// load/store aliasing — both >100 us per block). Column c of L is broadcast
-// through shared memory; the <= 63 updates of a step are independent FMAs.
-constexpr int kRot = 8;  // steps per register rotation
+// The 64 x 64 diagonal block at (k0, k0): Cholesky in place (lower) plus its
+// inverse Dinv = L11^-1 (64 x 64, row-major), which turns the panel TRSM into a
+// GEMM. 256 threads; thread t owns row i = t / 4, columns q4 + 4 j (q4 = t % 4,
+// j < 16) in registers. Column c is published through a double-buffered
+// shared vector, so each of the 64 right-looking steps costs ONE barrier,
+// one rsqrt (computed redundantly by every thread) and <= 16 independent
+// FMAs per thread; the inverse runs the same way over rows of L^-1. Loops
+// are runtime loops over groups of 4 columns with the register row ROTATED
+// by one group each time, so indices stay static and the code stays small
+// (straight-line versions were instruction-fetch bound).
+constexpr int LDP = NB + 1;
+constexpr int kLeafThreads = 256;
 
-__global__ void __launch_bounds__(NB) potrf_diag_kernel(double* G, int64_t ld, int k0, int nb,
-                                                         int* status, double* Dinv) {
-  // col[] is padded so the unpredicated updates may read past row 63: entries
-  // that land in a row's upper triangle are never used as factor values.
-  __shared__ double col[2 * NB + kRot];
-  __shared__ double lt[NB][NB + 1];  // lt[q][r] = L[r][q]
-  __shared__ double rl_s[kRot];
-  __shared__ int bad;
-  const int i = threadIdx.x;
-  double* grow = G + (int64_t)(k0 + i) * ld + k0;
-  double r[NB + kRot];  // r[k] = A[i][c0 + k] for the current rotation base c0
+// X = L^-1 for the lower 64 x 64 L in Lsm (rinv[q] = 1 / L_qq); this
+// thread's entries X[i][q4 + 4j] come back in x. rowq: 2 x 64 scratch.
+SKB_DEV void leaf_inverse(const double (*Lsm)[LDP], const double* rinv, double (*rowq)[NB],
+                          double (&x)[16]) {
+  const int t = threadIdx.x, i = t >> 2, q4 = t & 3;
 #pragma unroll
-  for (int k = 0; k < NB; ++k) r[k] = k <= i ? grow[k] : 0.0;
+  for (int j = 0; j < 16; ++j) x[j] = (q4 + 4 * j == i) ? 1.0 : 0.0;
+#pragma unroll 2
+  for (int q = 0; q < NB; ++q) {
+    const int buf = q & 1;
+    if (i == q) {
+      const double rq = rinv[q];
 #pragma unroll
-  for (int k = NB; k < NB + kRot; ++k) r[k] = 0.0;
-  for (int k = i; k < 2 * NB + kRot; k += NB) col[k] = 0.0;
-  if (i == 0) bad = 0;
-  __syncthreads();
-  for (int c0 = 0; c0 < NB; c0 += kRot) {
-#pragma unroll
-    for (int u = 0; u < kRot; ++u) {
-      const int c = c0 + u;
-      if (i == c) {
-        const double piv = r[u];
-        if (!(piv > 0.0)) bad = 1;
-        const double l = sqrt(piv);
-        col[c] = l;
-        rl_s[u] = 1.0 / l;
+      for (int j = 0; j < 16; ++j) {
+        x[j] *= rq;
+        rowq[buf][q4 + 4 * j] = x[j];
       }
-      __syncthreads();
-      if (bad) break;
-      double lic = 0.0;
-      if (i > c) {
-        lic = r[u] * rl_s[u];
-        col[i] = lic;
-      }
-      __syncthreads();
-      if (i >= c) {
-        const double v = i == c ? col[c] : lic;
-        grow[c] = v;
-        lt[c][i] = v;
-      }
-#pragma unroll
-      for (int k = u + 1; k < NB + u; ++k) r[k] -= lic * col[c0 + k];  // lic == 0 for i <= c
-      __syncthreads();
     }
-    if (bad) break;
+    __syncthreads();
+    if (i > q) {
+      const double lkq = Lsm[i][q];
 #pragma unroll
-    for (int k = 0; k < NB; ++k) r[k] = r[k + kRot];
+      for (int j = 0; j < 16; ++j)
+        if (q4 + 4 * j <= q) x[j] = fma(-lkq, rowq[buf][q4 + 4 * j], x[j]);
+    }
   }
-  if (bad) {
-    if (i == 0) atomicOr(status, ST_CHOL_FAIL);
+}
+
+__global__ void __launch_bounds__(kLeafThreads) potrf_diag_kernel(double* G, int64_t ld, int k0,
+                                                                   int nb, int* status,
+                                                                   double* Dinv) {
+  __shared__ double Lsm[NB][LDP];
+  __shared__ double colc[2][NB];
+  __shared__ double rinv[NB];
+  __shared__ int bad_s;
+  const int t = threadIdx.x, i = t >> 2, q4 = t & 3;
+  double* B = G + (int64_t)k0 * ld + k0;
+  double r[16];  // r[j] = A[i][q4 + 4 (j + g)] in column group g
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int k = q4 + 4 * j;
+    r[j] = k <= i ? B[(int64_t)i * ld + k] : 0.0;
+    Lsm[i][k] = 0.0;
+  }
+  if (t == 0) bad_s = 0;
+  for (int c0 = 0; c0 < NB; c0 += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u, buf = u & 1;
+      if (q4 == u && i >= c) colc[buf][i] = r[0];
+      __syncthreads();
+      const double piv = colc[buf][c];
+      const double rs = rsqrt(piv);
+      if (t == 0) {
+        if (!(piv > 0.0)) bad_s = 1;
+        rinv[c] = rs;
+      }
+      const double ai = colc[buf][i];
+      if (q4 == u && i >= c) Lsm[i][c] = i == c ? piv * rs : ai * rs;
+      if (i > c) {
+        const double air = ai * (rs * rs);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int k = q4 + 4 * j + c0;  // column of r[j]
+          if (k > c && k <= i) r[j] = fma(-air, colc[buf][k], r[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 15; ++j) r[j] = r[j + 1];
+    r[15] = 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int k = q4 + 4 * j;
+    B[(int64_t)i * ld + k] = Lsm[i][k];
+  }
+  if (bad_s) {
+    if (t == 0) atomicOr(status, ST_CHOL_FAIL);
     return;
   }
-  for (int k = i + 1; k < NB; ++k) grow[k] = 0.0;
   if (!Dinv) return;
-  // Column i of L11^-1 by right-looking forward substitution, rotated the same
-  // way: x[u] is entry q = q0 + u; x_q /= L_qq, then x_{q+k} -= L_{q+k,q} x_q.
-  double x[NB + kRot];
+  double x[16];
+  leaf_inverse(Lsm, rinv, colc, x);
 #pragma unroll
-  for (int k = 0; k < NB + kRot; ++k) x[k] = 0.0;
-  x[0] = 1.0;
-  const int q_start = i & ~(kRot - 1);  // entries above i stay zero
-#pragma unroll
-  for (int k = 0; k < NB; ++k) x[k] = (k == i - q_start) ? 1.0 : 0.0;
-  for (int q = 0; q < q_start; ++q) Dinv[(int64_t)q * NB + i] = 0.0;
-  for (int q0 = q_start; q0 < NB; q0 += kRot) {
-#pragma unroll
-    for (int u = 0; u < kRot; ++u) {
-      const int q = q0 + u;
-      const double x0 = q < i ? 0.0 : x[u] / lt[q][q];
-      Dinv[(int64_t)q * NB + i] = x0;
-#pragma unroll
-      for (int k = u + 1; k < NB + u; ++k)
-        if (q0 + k < NB) x[k] -= lt[q][q0 + k] * x0;
-    }
-#pragma unroll
-    for (int k = 0; k < NB; ++k) x[k] = x[k + kRot];
-  }
+  for (int j = 0; j < 16; ++j) Dinv[i * NB + q4 + 4 * j] = x[j];
 }
 
 // Panel: rows i in [k0+nb, M) of columns [k0, k0+nb): solve x L11' = a by
@@ -505,30 +530,27 @@ __global__ void __launch_bounds__(128) trsm_panel_kernel(double* G, int64_t ld, 
 }
 
 // Inverse of each 64x64 lower-triangular diagonal block: Linv[b] = L[b]^-1.
-__global__ void __launch_bounds__(64) trtri_diag_kernel(const double* L, double* Li, int64_t ld) {
-  __shared__ double l[NB][NB + 1];
-  const int b0 = blockIdx.x * NB;
-  for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-    const int i = t / NB, j = t % NB;
-    l[i][j] = L[(int64_t)(b0 + i) * ld + b0 + j];
+// Inverses of the 64 x 64 diagonal blocks of a lower-triangular L (one CTA
+// per block), with the row-parallel scheme of potrf_diag_kernel.
+__global__ void __launch_bounds__(kLeafThreads) trtri_diag_kernel(const double* L, double* Li,
+                                                                   int64_t ld) {
+  __shared__ double Lsm[NB][LDP];
+  __shared__ double rowq[2][NB];
+  __shared__ double rinv[NB];
+  const int t = threadIdx.x, i = t >> 2, q4 = t & 3;
+  const int64_t b0 = (int64_t)blockIdx.x * NB;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int k = q4 + 4 * j;
+    Lsm[i][k] = k <= i ? L[(b0 + i) * ld + b0 + k] : 0.0;
   }
   __syncthreads();
-  const int j = threadIdx.x;  // column of the inverse
-  double x[NB];
+  if (t < NB) rinv[t] = 1.0 / Lsm[t][t];
+  __syncthreads();
+  double x[16];
+  leaf_inverse(Lsm, rinv, rowq, x);
 #pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    double t = (i == j) ? 1.0 : 0.0;
-    if (i < j) {
-      x[i] = 0.0;
-      continue;
-    }
-#pragma unroll
-    for (int q = 0; q < i; ++q)
-      if (q >= j) t -= l[i][q] * x[q];
-    x[i] = t / l[i][i];
-  }
-#pragma unroll
-  for (int i = 0; i < NB; ++i) Li[(int64_t)(b0 + i) * ld + b0 + j] = x[i];
+  for (int j = 0; j < 16; ++j) Li[(b0 + i) * ld + b0 + q4 + 4 * j] = x[j];
 }
 
 __global__ void set_identity_pad_kernel(double* G, int64_t ld, int m, int Mp) {
@@ -784,11 +806,7 @@ extern "C" int skb_set_identity_pad(double* G, int64_t ld, int32_t m, int32_t Mp
   return skb_launch_status(__func__);
 }
 
-static int round_pad(int m) {
-  int p = NB;
-  while (p < m) p <<= 1;
-  return p;
-}
+static int round_pad(int m) { return std::max(NB, (m + NB - 1) / NB * NB); }
 
 extern "C" int32_t skb_factor_padded_dim(int32_t m) { return round_pad(m); }
 
@@ -801,12 +819,13 @@ static int potrf(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStr
   double* Dinv = (double*)skb_ws_take(ws, (size_t)NB * NB * 8);
   if (!Dinv) return SKB_ERR_WORKSPACE;
   for (int k0 = 0; k0 < Mp; k0 += NB) {
-    potrf_diag_kernel<<<1, NB, 0, st>>>(G, ld, k0, NB, status, Dinv);
+    potrf_diag_kernel<<<1, kLeafThreads, 0, st>>>(G, ld, k0, NB, status, Dinv);
     const int rest = Mp - k0 - NB;
     if (rest <= 0) break;
     double* P = G + (int64_t)(k0 + NB) * ld + k0;
     double* T = G + (int64_t)(k0 + NB) * ld + k0 + NB;
     GemmArgs gp = gemm_args(P, ld, 0, Dinv, NB, 1, P, ld, rest, NB, NB, 1.0, 0.0, 0);
+    gp.tri_b = 2;  // opB = Dinv' (upper)
     int rc = gemm_launch(gp, 1, ws, st);
     if (rc) return rc;
     GemmArgs g = gemm_args(P, ld, 0, P, ld, 1, T, ld, rest, rest, NB, -1.0, 1.0, 1);
@@ -828,32 +847,52 @@ extern "C" int skb_potrf(double* G, int64_t ld, int32_t Mp, int* status, void* w
   return skb_launch_status(__func__);
 }
 
-// Li = L^-1 for lower-triangular L (Mp = 64 * 2^k, ld), by recursive doubling:
-// inv([A 0; B C]) = [A^-1 0; -C^-1 B A^-1  C^-1], all pairs of a level batched.
+// Li = L^-1 for lower-triangular L (Mp = 64 q, ld), by recursive doubling:
+// inv([A 0; B C]) = [A^-1 0; -C^-1 B A^-1  C^-1]. Level h merges aligned
+// pairs of h-blocks (all full pairs of a level batched); a trailing partial
+// block (Mp not a multiple of 2h) is merged with its left neighbour on its
+// own. Triangular operands trim each tile's k range (about half the flops).
 static int trtri(const double* L, double* Li, int64_t ld, int Mp, skb_ws* ws, cudaStream_t st) {
   cudaMemsetAsync(Li, 0, (size_t)Mp * ld * 8, st);
-  trtri_diag_kernel<<<Mp / NB, NB, 0, st>>>(L, Li, ld);
+  trtri_diag_kernel<<<Mp / NB, kLeafThreads, 0, st>>>(L, Li, ld);
   const size_t mark = ws->off;
-  double* T = (double*)skb_ws_take(ws, (size_t)Mp * Mp / 2 * 8);
+  double* T = (double*)skb_ws_take(ws, (size_t)Mp * Mp / 2 * 8 + 64);
   if (!T) return SKB_ERR_WORKSPACE;
   for (int h = NB; h < Mp; h <<= 1) {
     const int pairs = Mp / (2 * h);
+    const int rem = Mp - pairs * 2 * h;
+    const int h2 = rem > h ? rem - h : 0;  // size of a trailing partial right block
     const int64_t s = (int64_t)2 * h * (ld + 1);  // diagonal stride between pairs
-    // T_p = L21_p * Li11_p  (h x h each), T stored contiguous h x h per pair
-    GemmArgs g1 = gemm_args(L + (int64_t)h * ld, ld, 0, Li, ld, 0, T, h, h, h, h, 1.0, 0.0, 0);
-    g1.sA = s;
-    g1.sB = s;
-    g1.sC = (int64_t)h * h;
-    int rc = gemm_launch(g1, pairs, ws, st);
-    if (rc) return rc;
-    // Li21_p = -Li22_p * T_p
-    GemmArgs g2 = gemm_args(Li + (int64_t)h * ld + h, ld, 0, T, h, 0, Li + (int64_t)h * ld, ld, h,
-                            h, h, -1.0, 0.0, 0);
-    g2.sA = s;
-    g2.sB = (int64_t)h * h;
-    g2.sC = s;
-    rc = gemm_launch(g2, pairs, ws, st);
-    if (rc) return rc;
+    int rc;
+    if (pairs) {
+      // T_p = L21_p * Li11_p  (h x h each), T stored contiguous h x h per pair
+      GemmArgs g1 = gemm_args(L + (int64_t)h * ld, ld, 0, Li, ld, 0, T, h, h, h, h, 1.0, 0.0, 0);
+      g1.sA = s;
+      g1.sB = s;
+      g1.sC = (int64_t)h * h;
+      g1.tri_b = 1;
+      if ((rc = gemm_launch(g1, pairs, ws, st))) return rc;
+      // Li21_p = -Li22_p * T_p
+      GemmArgs g2 = gemm_args(Li + (int64_t)h * ld + h, ld, 0, T, h, 0, Li + (int64_t)h * ld, ld,
+                              h, h, h, -1.0, 0.0, 0);
+      g2.sA = s;
+      g2.sB = (int64_t)h * h;
+      g2.sC = s;
+      g2.tri_a = 1;
+      if ((rc = gemm_launch(g2, pairs, ws, st))) return rc;
+    }
+    if (h2) {
+      const int64_t o = (int64_t)pairs * 2 * h;
+      double* T2 = T + (size_t)pairs * h * h;
+      GemmArgs g1 = gemm_args(L + (o + h) * ld + o, ld, 0, Li + o * ld + o, ld, 0, T2, h, h2, h, h,
+                              1.0, 0.0, 0);
+      g1.tri_b = 1;
+      if ((rc = gemm_launch(g1, 1, ws, st))) return rc;
+      GemmArgs g2 = gemm_args(Li + (o + h) * ld + o + h, ld, 0, T2, h, 0, Li + (o + h) * ld + o, ld,
+                              h2, h, h2, -1.0, 0.0, 0);
+      g2.tri_a = 1;
+      if ((rc = gemm_launch(g2, 1, ws, st))) return rc;
+    }
   }
   ws->off = mark;
   return skb_launch_status(__func__);
@@ -861,7 +900,7 @@ static int trtri(const double* L, double* Li, int64_t ld, int Mp, skb_ws* ws, cu
 
 extern "C" int skb_trtri(const double* L, double* Li, int64_t ld, int32_t Mp, void* workspace,
                          size_t ws_bytes, void* stream) {
-  if (Mp % NB || (Mp & (Mp - 1))) return SKB_ERR_ARG;
+  if (Mp % NB || Mp <= 0) return SKB_ERR_ARG;
   skb_ws ws = skb_ws_make(workspace, ws_bytes);
   return trtri(L, Li, ld, Mp, &ws, (cudaStream_t)stream);
 }
@@ -936,6 +975,7 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
   for (int p = 0; p < passes; ++p) {
     // Y = Z * L1i'  (w x m)
     GemmArgs gy = gemm_args(Z, ldx, 0, L1i, ld, 1, Y, ldx, w, m, m, 1.0, 0.0, 0);
+    gy.tri_b = 2;  // opB = L1i' (upper)
     if ((rc = gemm_launch(gy, 1, &ws, st))) return rc;
     Z = Y;
     if ((rc = gram(Y))) return rc;
@@ -945,6 +985,8 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
     // Linv = L2i * L1i (lower x lower; tiles above the diagonal are skipped -> clear first)
     cudaMemsetAsync(Linv, 0, MM * 8, st);
     GemmArgs gi = gemm_args(L2i, ld, 0, L1i, ld, 0, Linv, ld, Mp, Mp, Mp, 1.0, 0.0, 1);
+    gi.tri_a = 1;  // lower x lower
+    gi.tri_b = 1;
     if ((rc = gemm_launch(gi, 1, &ws, st))) return rc;
     if (p + 1 < passes) {
       // next pass factors X again: L1i <- Linv (cumulative inverse), Y = X Linv'
