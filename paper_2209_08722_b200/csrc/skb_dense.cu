@@ -668,14 +668,18 @@ __global__ void __launch_bounds__(256) rowdot_gemv_kernel(const double* __restri
   const int i = warp;
   const int lo = tri == 2 ? i : 0, hi = tri == 1 ? min(i + 1, cols) : cols;
   const double* row = Mx + (int64_t)i * ld;
-  double s0 = 0.0, s1 = 0.0;
+  // 8 independent 256-byte loads in flight per warp (latency-bound at m ~ 1e3)
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int k = lo + lane;
-  for (; k + 32 < hi; k += 64) {
-    s0 = fma(row[k], x[k], s0);
-    s1 = fma(row[k + 32], x[k + 32], s1);
+  for (; k + 7 * 32 < hi; k += 8 * 32) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = fma(__ldg(&row[k + 32 * u]), __ldg(&x[k + 32 * u]), acc[u]);
   }
-  if (k < hi) s0 = fma(row[k], x[k], s0);
-  const double s = warp_sum(s0 + s1);
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (k + 32 * u < hi) acc[u] = fma(__ldg(&row[k + 32 * u]), __ldg(&x[k + 32 * u]), acc[u]);
+  const double s = warp_sum(((acc[0] + acc[1]) + (acc[2] + acc[3])) +
+                            ((acc[4] + acc[5]) + (acc[6] + acc[7])));
   if (lane == 0) y[i] = s;
 }
 

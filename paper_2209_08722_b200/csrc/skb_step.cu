@@ -52,13 +52,25 @@ SKB_DEV void grid_reduce(double (&v)[K], const int (&ops)[K], double* part, unsi
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
+  __syncthreads();  // (also orders the sm[] reuse below)
   if (!last) return;
   __threadfence();
+  // last block: every thread folds a fixed strided subset of the partials,
+  // then a block reduction (deterministic for a given grid size)
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = red_init(ops[k]);
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += kRedThreads)
+      x = red_comb(ops[k], x, __ldcg(&part[(size_t)b * K + k]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = red_comb(ops[k], x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) sm[wid][k] = x;
+  }
+  __syncthreads();
   if (threadIdx.x < K) {
     const int k = threadIdx.x;
-    double x = red_init(ops[k]);
-    for (unsigned b = 0; b < gridDim.x; ++b) x = red_comb(ops[k], x, part[(size_t)b * K + k]);
+    double x = sm[0][k];
+    for (int w = 1; w < kRedThreads / 32; ++w) x = red_comb(ops[k], x, sm[w][k]);
     out[k] = x;
   }
   if (threadIdx.x == 0) *ticket = 0;  // reusable
@@ -274,21 +286,23 @@ __global__ void sub_kernel(const double* __restrict__ a, const double* __restric
 
 using namespace skb;
 
+constexpr int kRedBlocksPerSm = 8;  // full occupancy: enough loads in flight for HBM
+
 static int red_grid(int64_t n) {
   int64_t g = (n + kRedThreads - 1) / kRedThreads;
-  const int64_t cap = 2 * (int64_t)skb_num_sms();
+  const int64_t cap = kRedBlocksPerSm * (int64_t)skb_num_sms();
   return (int)(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
 // Reduction scratch: partials (grid * 16 doubles) + ticket.
 extern "C" size_t skb_reduce_workspace_bytes(void) {
-  return (size_t)2 * skb_num_sms() * 32 * 8 + 512;
+  return (size_t)kRedBlocksPerSm * skb_num_sms() * 32 * 8 + 512;
 }
 
 #define RED_WS                                                                   \
   skb_ws ws = skb_ws_make(workspace, ws_bytes);                                  \
   unsigned* ticket = (unsigned*)skb_ws_take(&ws, 256);                           \
-  double* part = (double*)skb_ws_take(&ws, (size_t)2 * skb_num_sms() * 16 * 8); \
+  double* part = (double*)skb_ws_take(&ws, (size_t)kRedBlocksPerSm * skb_num_sms() * 32 * 8); \
   if (!ticket || !part) return SKB_ERR_WORKSPACE;                                \
   cudaStream_t st = (cudaStream_t)stream
 
