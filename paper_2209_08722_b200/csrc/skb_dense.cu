@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmArgs g) {
   extern __shared__ __align__(16) double psm[];
   using TAt = PTileA<TA>;
   using TBt = PTileB<TB>;
-  constexpr int kStage = TAt::kSize + TBt::kSize;
+  constexpr int kStage = TAt::kSize + TBt::kSize + PBK;  // + the k-tile's kscale
   const int batch = blockIdx.z / g.splits, split = blockIdx.z % g.splits;
   const int bm = blockIdx.y, bn = blockIdx.x;
   if (g.lower_only && bn * PBN > bm * PBM + PBM - 1) return;
@@ -288,6 +288,11 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmArgs g) {
       }
       cp_async16(dst, src, bytes);
     }
+    if (g.kscale && tid < PBK / 2) {  // the k-tile's 16 scale factors ride along
+      const int gk = k0 + 2 * tid;
+      const int bytes = max(0, min(16, (k_end - gk) * 8));
+      cp_async16(Bs + TBt::kSize + 2 * tid, bytes ? g.kscale + gk : g.kscale, bytes);
+    }
   };
 
   double acc[4][4][2];
@@ -308,7 +313,6 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmArgs g) {
     cp_async_commit();
     const double* As = psm + (t % PST) * kStage;
     const double* Bs = As + TAt::kSize;
-    const int k0 = k_begin + t * PBK;
 #pragma unroll
     for (int kk = 0; kk < PBK; kk += 4) {
       double af[4], bf[4];
@@ -321,8 +325,7 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmArgs g) {
         bf[b] = TB ? Bs[(wn + b * 8 + gq) * TBt::kStride + kk + tq]
                    : Bs[(kk + tq) * TBt::kStride + wn + b * 8 + gq];
       if (g.kscale) {
-        const int gk = k0 + kk + tq;
-        const double sc = gk < k_end ? g.kscale[gk] : 0.0;
+        const double sc = Bs[TBt::kSize + kk + tq];  // zero-filled past k_end
 #pragma unroll
         for (int a = 0; a < 4; ++a) af[a] *= sc;
       }
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmArgs g) {
 
 template <int TA, int TB>
 static size_t pipe_smem_bytes() {
-  return (size_t)PST * (PTileA<TA>::kSize + PTileB<TB>::kSize) * sizeof(double);
+  return (size_t)PST * (PTileA<TA>::kSize + PTileB<TB>::kSize + PBK) * sizeof(double);
 }
 
 template <int TA, int TB>
@@ -379,7 +382,7 @@ static bool pipe_ok(const GemmArgs& g) {
   if (getenv("SKB_GEMM_NOPIPE")) return false;
   auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   return al(g.A) && al(g.B) && (g.lda % 2 == 0) && (g.ldb % 2 == 0) && (g.sA % 2 == 0) &&
-         (g.sB % 2 == 0);
+         (g.sB % 2 == 0) && (!g.kscale || al(g.kscale));
 }
 
 __global__ void gemm_splitk_reduce_kernel(GemmArgs g, int nbatch) {
@@ -706,6 +709,21 @@ static int gemm_launch(const GemmArgs& base, int nbatch, skb_ws* ws, cudaStream_
     const size_t per = (size_t)nbatch * g.M * g.N * 8;
     const size_t avail = ws->cap > ws->off + 512 ? ws->cap - ws->off - 512 : 0;
     while (splits > 1 && per * splits > avail) --splits;
+  } else if (g.K >= 4096 && !g.lower_only) {
+    // many tiles but a long K: split to fill the last wave (e.g. 512 tiles on
+    // 296 slots run at 86%; 4 splits at 99%)
+    const auto eff = [&](int sp) {
+      const long c = (long)tiles * sp, w = (c + target - 1) / target;
+      return (double)c / (double)(w * target);
+    };
+    const size_t per = (size_t)nbatch * g.M * g.N * 8;
+    const size_t avail = ws->cap > ws->off + 512 ? ws->cap - ws->off - 512 : 0;
+    double best = eff(1);
+    for (int sp = 2; sp <= 8 && g.K / sp >= 512; ++sp)
+      if (eff(sp) > best + 0.05 && per * sp <= avail) {
+        best = eff(sp);
+        splits = sp;
+      }
   }
   g.splits = splits;
   g.kchunk = (((g.K + splits - 1) / splits) + GBK - 1) / GBK * GBK;

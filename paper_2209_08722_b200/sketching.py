@@ -162,7 +162,8 @@ def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = 
                       ldx, ws, cap, stream_ptr())
     else:  # dense Gaussian: one DMMA GEMM, X = W' D A' (sketching.py:158-159)
         Ad = lp.dense_A()
-        ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, W.w)))
+        # + room for up to 8 split-K partials of the w x m product
+        ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, W.w)) + 8 * 8 * m * W.w)
         _lib.call("skb_gaussian_apply", Ad.cols, m, Ad.n, Ad.lda, d, W.dense, W.w, X, ldx, ws,
                   cap, stream_ptr())
     if ldx != m:
