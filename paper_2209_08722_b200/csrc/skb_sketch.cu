@@ -390,6 +390,49 @@ __global__ void __launch_bounds__(32)
   }
 }
 
+// ---- CSC A, large m: one THREAD per bucket, its row of X (bucket-major, zeroed
+// beforehand) updated in place in global memory. The thread walks the
+// bucket's members in ascending j and applies each member's entries in
+// order, so every (row, bucket) sum is the same left-to-right fl-sum as
+// scipy's (bit-exact); buckets are independent, so all w threads run at once
+// (a shared-memory m-vector per bucket would allow only ~2 buckets per SM at
+// m = 1e4). Index loads of the next member are issued ahead of the RMWs.
+constexpr int kRmwThreads = 128;
+constexpr int kRmwStage = 8;
+
+__global__ void __launch_bounds__(kRmwThreads)
+    csc_sketch_rmw_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                          const double* __restrict__ av, const double* __restrict__ d,
+                          const uint64_t* __restrict__ start, const int32_t* __restrict__ mem_e,
+                          const double* __restrict__ wvals, int s, int w,
+                          double* __restrict__ X, int64_t ldx) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= w) return;
+  double* __restrict__ Xb = X + (int64_t)b * ldx;
+  const uint64_t e0 = start[b], e1 = start[b + 1];
+  int64_t ei_next = e0 < e1 ? mem_e[e0] : 0;
+  for (uint64_t e = e0; e < e1; ++e) {
+    const int64_t ei = ei_next;
+    if (e + 1 < e1) ei_next = mem_e[e + 1];
+    const int64_t j = ei / s;
+    const double wv = wvals[ei], dj = d[j];
+    const int64_t c0 = colptr[j], c1 = colptr[j + 1];
+    for (int64_t t0 = c0; t0 < c1; t0 += kRmwStage) {
+      int r[kRmwStage];
+      double a[kRmwStage];
+#pragma unroll
+      for (int q = 0; q < kRmwStage; ++q) {
+        const bool ok = t0 + q < c1;
+        r[q] = ok ? rowidx[t0 + q] : 0;
+        a[q] = ok ? av[t0 + q] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kRmwStage; ++q)
+        if (t0 + q < c1) Xb[r[q]] = __dadd_rn(Xb[r[q]], __dmul_rn(__dmul_rn(a[q], dj), wv));
+    }
+  }
+}
+
 extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx,
                                     const double* av, int64_t m, int64_t n, const double* d,
                                     const int32_t* cols, const double* vals, int32_t s, int32_t w,
@@ -403,6 +446,12 @@ extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx
   unsigned int* counter;
   int rc = bucket_sort(cols, n, s, w, &ws, st, &start, &mem_e, &counter);
   if (rc) return rc;
+  if (m > 2048) {
+    cudaMemsetAsync(X, 0, (size_t)w * ldx * 8, st);
+    csc_sketch_rmw_kernel<<<(w + kRmwThreads - 1) / kRmwThreads, kRmwThreads, 0, st>>>(
+        colptr, rowidx, av, d, start, mem_e, vals, s, w, X, ldx);
+    return skb_launch_status(__func__);
+  }
   const size_t smem = (size_t)m * 8 + 32 * kCscStage * 4 + 32 * 4 + 16 + 32 * kCscStage * 8;
   if (smem > 220 * 1024) return SKB_ERR_UNSUPPORTED;
   static size_t conf = 0;
