@@ -442,6 +442,125 @@ __global__ void __launch_bounds__(kCoopThreads, KP <= 8 ? 2 : 1)
   }
 }
 
+// ------------------------------------------------------ warp-pair variant
+// For 1024 < m <= 2048 (c3: m = 2000): two warps stream the SAME column, each
+// owning half of its rows (1024 rows = 16 row pairs per lane, z and the
+// m-vector partial in registers as in colstream_kernel). A pair has its own
+// TMA ring (one column per stage, one cp.async.bulk); the two half-dots meet
+// in shared memory behind a 64-thread named barrier, then both warps re-read
+// their half from the stage for the rank-1 update. 4 pairs per CTA, one CTA
+// per SM: only pair-local barriers, unlike the CTA-wide lockstep of
+// colcoop_kernel.
+constexpr int kPairR2 = 16;
+constexpr int kPairHalf = 64 * kPairR2;  // rows per warp
+
+SKB_DEV void pair_bar(int id) { asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory"); }
+
+template <class Op>
+__global__ void __launch_bounds__(256, 1)
+    colpair_kernel(const double* __restrict__ A, int64_t lda, int m, int64_t n, int stages,
+                   int half, const double* __restrict__ z, double* __restrict__ part, Op op,
+                   const int* __restrict__ gate) {
+  if (gate && *gate) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int pair = warp >> 1, h = warp & 1;
+  const size_t col_bytes = (size_t)lda * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);               // [4][stages]
+  double* dots = reinterpret_cast<double*>(smem + 8 * 4 * 8);         // [4][2]
+  unsigned char* bufs = smem + 512;
+  unsigned char* mybuf = bufs + (size_t)pair * stages * col_bytes;
+  uint64_t* mybar = full + pair * stages;
+  if (tid == 0) {
+    for (int q = 0; q < 4 * stages; ++q) mbar_init(&full[q], 1);
+    fence_mbar_init();
+  }
+  double zr[2 * kPairR2], acc[2 * kPairR2];
+  // warp h owns rows [h * half, min(m, (h + 1) * half)), half = ceil(m / 2) rounded to 64
+  const int rbase = h * half + 2 * lane;
+  const int rend = min(m, (h + 1) * half);
+#pragma unroll
+  for (int k = 0; k < kPairR2; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int r = rbase + 64 * k + e;
+      zr[2 * k + e] = (Op::kDot && r < rend) ? z[r] : 0.0;
+      acc[2 * k + e] = 0.0;
+    }
+  }
+  __syncthreads();
+  const int64_t gp = (int64_t)blockIdx.x * 4 + pair, GP = (int64_t)gridDim.x * 4;
+  const int64_t my = gp < n ? (n - 1 - gp) / GP + 1 : 0;
+  const uint64_t pol = l2_evict_first_policy();
+  const bool producer = h == 0 && lane == 0;
+  auto issue = [&](int64_t i, int st) {
+    const int64_t j = gp + i * GP;
+    mbar_arrive_expect_tx(&mybar[st], (uint32_t)col_bytes);
+    bulk_g2s(mybuf + st * col_bytes, A + j * lda, (uint32_t)col_bytes, &mybar[st], pol);
+  };
+  if (producer)
+    for (int64_t i = 0; i < min((int64_t)stages, my); ++i) issue(i, (int)i);
+  const int bar_id = 1 + pair;
+  for (int64_t i = 0; i < my; ++i) {
+    const int st = (int)(i % stages);
+    const uint32_t ph = (uint32_t)((i / stages) & 1);
+    const int64_t j = gp + i * GP;
+    Pre pre;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) pre.v[q] = 0.0;
+    op.load(j, pre);
+    mbar_wait(&mybar[st], ph);
+    const double* col = reinterpret_cast<const double*>(mybuf + st * col_bytes);
+    double dot = 0.0;
+    if (Op::kDot) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < kPairR2; ++k) {
+        const int r = rbase + 64 * k;
+        if (r < rend) {
+          const double2 a = *reinterpret_cast<const double2*>(col + r);
+          d0 = fma(a.x, zr[2 * k], d0);
+          d1 = fma(r + 1 < rend ? a.y : 0.0, zr[2 * k + 1], d1);
+        }
+      }
+      const double sh = warp_sum(d0 + d1);
+      if (lane == 0) dots[pair * 2 + h] = sh;
+      pair_bar(bar_id);
+      dot = dots[pair * 2] + dots[pair * 2 + 1];
+    }
+    const double cf = op.coef(j, pre, dot);
+    if (producer) op.emit(j, pre, dot, cf);
+    if (Op::kAxpy) {
+#pragma unroll
+      for (int k = 0; k < kPairR2; ++k) {
+        const int r = rbase + 64 * k;
+        if (r < rend) {
+          const double2 a = *reinterpret_cast<const double2*>(col + r);
+          acc[2 * k] = fma(cf, a.x, acc[2 * k]);
+          acc[2 * k + 1] = fma(cf, r + 1 < rend ? a.y : 0.0, acc[2 * k + 1]);
+        }
+      }
+    }
+    pair_bar(bar_id);  // both halves done with the stage (and with dots)
+    if (producer && i + stages < my) issue(i + stages, st);
+  }
+  if (!Op::kAxpy) return;
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(bufs);  // [4][m]
+#pragma unroll
+  for (int k = 0; k < kPairR2; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int r = rbase + 64 * k + e;
+      if (r < rend) red[(size_t)pair * m + r] = acc[2 * k + e];
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < m; r += blockDim.x)
+    part[(size_t)blockIdx.x * m + r] =
+        (red[r] + red[(size_t)m + r]) + (red[2 * (size_t)m + r] + red[3 * (size_t)m + r]);
+}
+
 // out[i] = sum_b part[b][i] (fixed order: 8 interleaved slices, combined in order) - sub[i]
 __global__ void reduce_partials_kernel(const double* __restrict__ part, int nb, int m,
                                        const double* __restrict__ sub, double* __restrict__ out,
@@ -494,7 +613,10 @@ constexpr int kCoopMaxM = 16384;
 static StreamCfg coop_cfg(int m, int64_t n, int64_t lda) {
   StreamCfg c;
   const size_t col_bytes = (size_t)lda * 8;
-  c.cb = (int)std::max<size_t>(1, std::min<size_t>(kCoopMaxCb, 32768 / col_bytes));
+  static const size_t cb_bytes = getenv("SKB_COOP_STAGE_KB")
+                                    ? (size_t)atoi(getenv("SKB_COOP_STAGE_KB")) * 1024
+                                    : 32768;
+  c.cb = (int)std::max<size_t>(1, std::min<size_t>(kCoopMaxCb, cb_bytes / col_bytes));
   const size_t stage_bytes = (size_t)c.cb * col_bytes;
   const size_t head = 256 + 8 * (8 * kCoopMaxCb + kCoopMaxCb * 6) + 128;
   // CTAs per SM: the CTA runs its stages in lockstep, so a second resident CTA
@@ -566,6 +688,34 @@ static int run_stream(const double* A, int64_t lda, int m, int64_t n, const doub
       }
     }
     return 0;
+  }
+  static const bool no_pair = getenv("SKB_NO_PAIR") != nullptr;
+  if (m > 1024 && m <= 2 * kPairHalf && !no_pair) {
+    const size_t col_bytes = (size_t)lda * 8;
+    int stages = (int)std::min<size_t>(6, (218 * 1024 - 512) / (4 * col_bytes));
+    if (stages >= 2) {
+      const size_t smem = 512 + std::max((size_t)4 * stages * col_bytes, (size_t)4 * m * 8);
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(skb_num_sms(), (n + 3) / 4));
+      double* part = part_ext;
+      if (Op::kAxpy && !part) {
+        part = (double*)skb_ws_take(ws, (size_t)grid * m * 8);
+        if (!part) return SKB_ERR_WORKSPACE;
+      }
+      if (nparts_out) *nparts_out = grid;
+      auto kern = colpair_kernel<Op>;
+      static size_t configured = 0;
+      if (smem > configured) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+          return SKB_ERR_CUDA;
+        configured = smem;
+      }
+      const int half = ((m + 1) / 2 + 63) / 64 * 64;
+      kern<<<grid, 256, smem, st>>>(A, lda, m, n, stages, half, z, part, op, gate);
+      if (Op::kAxpy && !part_ext)
+        reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, grid, m, sub, out, gate);
+      return skb_launch_status(__func__);
+    }
   }
   const StreamCfg c = m > 1024 ? coop_cfg(m, n, lda) : stream_cfg(m, n, lda);
   double* part = part_ext;
