@@ -1,6 +1,6 @@
 """GPU busy vs wall for a few c2 outer steps via torch.profiler (CUPTI kernel
 records; development aid)."""
-import os, sys, time
+import collections, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from torch.profiler import ProfilerActivity, profile
@@ -58,3 +58,17 @@ norm = sorted(e.device_time for e in evs if "OpNormal" in e.name)
 print("OpNormal durations (us): min %.1f  p10 %.1f  p50 %.1f  p90 %.1f  max %.1f" % (
     norm[0], norm[len(norm) // 10], norm[len(norm) // 2], norm[9 * len(norm) // 10], norm[-1]))
 print("gated-looking (<100 us):", sum(1 for t in norm if t < 100), "sum us", sum(t for t in norm if t < 100))
+# idle gaps between consecutive device ops (> 15 us), attributed to the op after the gap
+ops = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
+gaps = collections.Counter() if False else {}
+import collections as _c
+gsum = _c.Counter(); gcnt = _c.Counter()
+for (s0, e0, n0), (s1, e1, n1) in zip(ops, ops[1:]):
+    gap = s1 - e0
+    if gap > 15:
+        key = n0[:40] + " -> " + n1[:40]
+        gsum[key] += gap; gcnt[key] += 1
+tot = sum(gsum.values())
+print(f"idle gaps > 15 us: {tot / 1e3:.2f} ms total over 4 outer")
+for k, v in gsum.most_common(15):
+    print(f"{v / 1e3:8.3f} ms  n={gcnt[k]:4d}  {k}")
