@@ -81,6 +81,46 @@ class Comm:
         dist.all_gather(out, buf, group=self.group)
         return torch.cat([o[: j1 - j0] for o, (j0, j1) in zip(out, sizes)]).to(t.device)
 
+    def row_block(self, rows: int):
+        """[r0, r1) of this rank's block when `rows` rows are scattered in equal
+        chunks of ceil(rows / world) (the last ones may be short or empty)."""
+        chunk = -(-rows // self.world)
+        r0 = min(rows, self.rank * chunk)
+        return r0, min(rows, r0 + chunk)
+
+    def reduce_scatter_rows(self, X: torch.Tensor) -> torch.Tensor:
+        """Sum X (rows x k, identical shape on every rank) over ranks and keep
+        this rank's row block (row_block). One NCCL reduce-scatter (rows padded
+        to a multiple of world); gloo sums on the host and slices."""
+        rows = X.shape[0]
+        r0, r1 = self.row_block(rows)
+        if self.world == 1:
+            return X
+        if self.host_staging or not X.is_cuda:
+            self.allreduce_(X)
+            return X[r0:r1].contiguous()
+        chunk = -(-rows // self.world)
+        if chunk * self.world != rows:
+            pad = torch.zeros((chunk * self.world - rows,) + tuple(X.shape[1:]), dtype=X.dtype,
+                              device=X.device)
+            X = torch.cat([X, pad])
+        out = torch.empty((chunk,) + tuple(X.shape[1:]), dtype=X.dtype, device=X.device)
+        dist.reduce_scatter_tensor(out, X.contiguous(), group=self.group)
+        return out[: r1 - r0].contiguous()
+
+    def allgather_rows(self, t: torch.Tensor, rows: int) -> torch.Tensor:
+        """Inverse of the row-block split: every rank's block of a `rows`-long
+        vector (or rows x k array) concatenated in rank order."""
+        if self.world == 1:
+            return t
+        chunk = -(-rows // self.world)
+        dev = "cpu" if self.host_staging else t.device
+        buf = torch.zeros((chunk,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+        buf[: t.shape[0]].copy_(t)
+        out = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(out, buf, group=self.group)
+        return torch.cat(out)[:rows].to(t.device)
+
     def barrier(self):
         if self.world > 1:
             dist.barrier(group=self.group)

@@ -44,6 +44,7 @@ class PreconditionerFactor:
     diag_max: float
     shifted: bool
     sketch_tag: tuple | None = None
+    dist: tuple | None = None   # (w_total, r0, comm): X holds bucket rows [r0, r0 + X.n)
 
     @property
     def ld(self) -> int:
@@ -51,12 +52,14 @@ class PreconditionerFactor:
 
     @property
     def w(self) -> int:
-        return self.X.n
+        return self.dist[0] if self.dist is not None else self.X.n
 
 
 def build_preconditioner(X: DeviceMatrix, rank_tol: float = RANK_TOL,
                          sketch_tag: tuple | None = None) -> PreconditionerFactor:
     """Factor ADW (given as X = ADW'); raises RankDeficient like the reference."""
+    if getattr(X, "dist", None) is not None:
+        return _build_distributed(X, rank_tol, sketch_tag)
     m, w = X.m, X.n
     if w < m:
         raise RankDeficient(f"sketch width {w} below row count {m}")
@@ -78,6 +81,80 @@ def build_preconditioner(X: DeviceMatrix, rank_tol: float = RANK_TOL,
                                 sketch_tag)
 
 
+def _gemm(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower, ws, cap):
+    _lib.call("skb_gemm", ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower, 1, 0, 0,
+              0, ws, cap, stream_ptr())
+
+
+def _build_distributed(X: DeviceMatrix, rank_tol: float, sketch_tag) -> PreconditionerFactor:
+    """CholeskyQR2 of a bucket-row-distributed X = ADW': every
+    rank forms its block's Gram X_g'X_g, the m x m Grams are allreduced, the
+    Cholesky / triangular inverse run redundantly on the (identical) sum, and
+    Y_g = X_g L1^-T stays local — the O(w m^2) GEMM work is split across ranks,
+    only m x m matrices move. Same algorithm and fallback (shifted CholeskyQR3)
+    as skb_factor_cholqr2."""
+    w_total, r0, comm = X.dist
+    m, wb = X.m, X.n
+    if w_total < m:
+        raise RankDeficient(f"sketch width {w_total} below row count {m}")
+    Mp = int(_lib.lib().skb_factor_padded_dim(m))
+    dev = X.cols.device
+    ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, max(wb, 1))))
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def gram(Z):
+        G = torch.zeros((Mp, Mp), dtype=F64, device=dev)
+        if wb > 0:
+            _gemm(1, 0, m, m, wb, 1.0, Z.cols, Z.lda, Z.cols, Z.lda, 0.0, G, Mp, 1, ws, cap)
+        comm.allreduce_(G)
+        _lib.call("skb_set_identity_pad", G, Mp, m, Mp, stream_ptr())
+        return G
+
+    def chol(G):
+        status.zero_()
+        _lib.call("skb_potrf", G, Mp, Mp, status, ws, cap, stream_ptr())
+        return int(status.item())
+
+    G = gram(X)
+    shifted = False
+    if chol(G) & 4:  # shifted CholeskyQR: s = 11 (m w + m (m + 1)) u ||X||_F^2
+        shifted = True
+        fro = (X.cols[:, :m] * X.cols[:, :m]).sum().reshape(1)
+        comm.allreduce_(fro)
+        shift = 11.0 * (m * w_total + m * (m + 1)) * 1.1102230246251565e-16 * float(fro.item())
+        G = gram(X)
+        G.diagonal()[:m] += shift
+        if chol(G) & 4:
+            raise RankDeficient("Cholesky failed after the shifted CholeskyQR retry")
+    dprod = G.diagonal()[:m].abs().clone()
+    L1i = torch.empty((Mp, Mp), dtype=F64, device=dev)
+    _lib.call("skb_trtri", G, L1i, Mp, Mp, ws, cap, stream_ptr())
+    Linv = torch.zeros((Mp, Mp), dtype=F64, device=dev)
+    Y = DeviceMatrix(torch.zeros_like(X.cols), m)
+    for p in range(2 if shifted else 1):
+        if wb > 0:  # Y = X L1i' (local rows)
+            _gemm(0, 1, wb, m, m, 1.0, X.cols, X.lda, L1i, Mp, 0.0, Y.cols, Y.lda, 0, ws, cap)
+        G2 = gram(Y)
+        if chol(G2) & 4:
+            raise RankDeficient("second CholeskyQR pass lost positive definiteness")
+        dprod = dprod * G2.diagonal()[:m].abs()
+        L2i = torch.empty((Mp, Mp), dtype=F64, device=dev)
+        _lib.call("skb_trtri", G2, L2i, Mp, Mp, ws, cap, stream_ptr())
+        Linv.zero_()
+        _gemm(0, 0, Mp, Mp, Mp, 1.0, L2i, Mp, L1i, Mp, 0.0, Linv, Mp, 1, ws, cap)
+        if p == 0 and shifted:
+            L1i = Linv.clone()
+    LinvT = torch.empty_like(Linv)
+    _lib.call("skb_transpose", Linv, LinvT, Mp, Mp, stream_ptr())
+    dstat = torch.stack([dprod.min(), dprod.max()]).cpu().numpy()
+    dmin, dmax = float(dstat[0]), float(dstat[1])
+    if not (dmax > 0.0) or not np.isfinite(dmin) or dmin / dmax < rank_tol:
+        raise RankDeficient(
+            f"ADW numerically rank deficient: diagonal ratio {dmin / max(dmax, 1e-300):.3e}")
+    return PreconditionerFactor(Linv, LinvT, None, X, m, dmin, dmax, shifted, sketch_tag,
+                                dist=X.dist)
+
+
 def _tri_gemv(M: torch.Tensor, m: int, tri: int, x: torch.Tensor, y: torch.Tensor, gate=None):
     _lib.call("skb_rowdot_gemv", M, M.shape[1], m, m, tri, x, y, gate, stream_ptr())
 
@@ -95,8 +172,12 @@ def apply_inv(f: PreconditionerFactor, r: torch.Tensor, out: torch.Tensor | None
 def apply_pinv_adw(f: PreconditionerFactor, r: torch.Tensor) -> torch.Tensor:
     """(ADW)^+ r = ADW' Q^-1 r, a length-w vector (preconditioning.py:64-66)."""
     z = apply_inv(f, r)
-    u = torch.empty(f.w, dtype=F64, device=r.device)
-    _lib.call("skb_rowdot_gemv", f.X.cols, f.X.lda, f.w, f.m, 0, z, u, None, stream_ptr())
+    nb = f.X.n
+    u = torch.empty(nb, dtype=F64, device=r.device)
+    if nb > 0:
+        _lib.call("skb_rowdot_gemv", f.X.cols, f.X.lda, nb, f.m, 0, z, u, None, stream_ptr())
+    if f.dist is not None:  # bucket blocks -> the whole u on every rank
+        u = f.dist[2].allgather_rows(u, f.dist[0])
     return u
 
 
@@ -104,5 +185,15 @@ def reconstruct(f: PreconditionerFactor, u: torch.Tensor, sub=None) -> torch.Ten
     """ADW u [- sub] (= U diag(sigma) V_hat' u, correction.py:61), one pass over X."""
     from . import kernels as K
     out = torch.empty(f.m, dtype=F64, device=u.device)
-    K.gemv(f.X, u, out, sub=sub)
+    if f.dist is None:
+        K.gemv(f.X, u, out, sub=sub)
+        return out
+    w_total, r0, comm = f.dist
+    if f.X.n > 0:
+        K.gemv(f.X, u[r0:r0 + f.X.n].contiguous(), out)
+    else:
+        out.zero_()
+    comm.allreduce_(out)
+    if sub is not None:
+        out -= sub
     return out

@@ -22,6 +22,12 @@ from .errors import DimensionMismatch, InvalidDims, NonpositiveScaling
 from .runtime import F64, lda_for, require_cuda, stream_ptr, workspace
 
 
+# Sharded runs keep ADW' distributed by bucket blocks and build the factor from
+# the blocks (Gram allreduce) instead of allreducing the whole w x m sketch and
+# factoring it on every rank.
+DISTRIBUTED_FACTOR = True
+
+
 def philox_key(seed: int):
     """numpy Philox(seed) key = SeedSequence(seed).generate_state(2, uint64)."""
     k = np.random.SeedSequence(int(seed)).generate_state(2, np.uint64)
@@ -169,5 +175,13 @@ def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = 
     if ldx != m:
         X[:, m:].zero_()
     if lp.comm.active:
-        lp.comm.allreduce_(X)
+        if W.kind == "identity" or not DISTRIBUTED_FACTOR:
+            lp.comm.allreduce_(X)
+        else:
+            # ADW = sum_g A_g D_g W_g: reduce-scatter by bucket (row) blocks; the
+            # factor is then built from the blocks (preconditioning.py)
+            r0, _ = lp.comm.row_block(W.w)
+            Xd = K.DeviceMatrix(lp.comm.reduce_scatter_rows(X), m)
+            Xd.dist = (W.w, r0, lp.comm)
+            return Xd
     return K.DeviceMatrix(X, m)

@@ -45,7 +45,22 @@ def _worker(rank, world, port, q):
         ok_stats = (abs(st[0].item() - float(x @ x)) <= 1e-12 * float(x @ x)
                     and st[1].item() == x.max() and st[2].item() == x.min())
         gathered = comm.gather_columns(torch.from_numpy(x[j0:j1].copy()), n).numpy()
-        q.put((rank, err, ok_stats, bool(np.array_equal(gathered, x)), (j0, j1)))
+        # distributed sketch: reduce-scatter of the w x m partial by bucket blocks,
+        # Gram of the blocks summed, and the block vector gathered back (w = 11: uneven)
+        w = 11
+        Pall = np.random.default_rng(5).standard_normal((world, w, m))
+        P = torch.from_numpy(Pall[rank].copy())
+        total = Pall.sum(axis=0)
+        r0, r1 = comm.row_block(w)
+        blk = comm.reduce_scatter_rows(P.clone())
+        ok_rs = blk.shape == (r1 - r0, m) and np.allclose(blk.numpy(), total[r0:r1], atol=1e-14)
+        G = blk.T @ blk
+        comm.allreduce_(G)
+        ok_gram = np.allclose(G.numpy(), total.T @ total, rtol=1e-13, atol=1e-13)
+        u = comm.allgather_rows(torch.arange(r0, r1, dtype=torch.float64), w)
+        ok_ag = np.array_equal(u.numpy(), np.arange(w, dtype=np.float64))
+        q.put((rank, err, ok_stats, bool(np.array_equal(gathered, x)), (j0, j1),
+               ok_rs and ok_gram and ok_ag))
     finally:
         dist.destroy_process_group()
 
@@ -63,5 +78,5 @@ def test_sharded_host_logic_world2():
         assert p.exitcode == 0
     res.sort()
     assert res[0][4] == (0, 502) and res[1][4] == (502, 1003)
-    for _, err, ok_stats, ok_gather, _ in res:
-        assert err <= 1e-13 and ok_stats and ok_gather
+    for _, err, ok_stats, ok_gather, _, ok_dist in res:
+        assert err <= 1e-13 and ok_stats and ok_gather and ok_dist

@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, kind="sparse"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -40,8 +40,13 @@ def _rank_main(rank, world, port, q):
         comm = Comm()
         dlp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c), comm=comm)
         st = IC.make_iterate(dlp, lpd.x0, lpd.y0, lpd.s0)
-        rep = IC.solve(dlp, st, IC.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1),
-                                             sigma=0.5, w=160, s=4, tol_outer=1e-7, seed=3))
+        if kind == "gaussian":
+            prm = IC.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5,
+                               sketch="gaussian", w=160, tol_outer=1e-6, seed=9)
+        else:
+            prm = IC.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5, w=160, s=4,
+                               tol_outer=1e-7, seed=3)
+        rep = IC.solve(dlp, st, prm)
         q.put((rank, rep.outer, [r.inner_iterations for r in rep.steps], rep.mu_trace,
                rep.objective, rep.x.shape[0], [r.sketch_seed for r in rep.steps]))
     except Exception as e:  # surface the failure to the parent
@@ -51,22 +56,30 @@ def _rank_main(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_sharded_solve_world2_matches_reference():
+@pytest.mark.parametrize("world,kind", [(2, "sparse"), (3, "sparse"), (2, "gaussian")])
+def test_sharded_solve_matches_reference(world, kind):
+    """Sharded sketch + distributed CholeskyQR2 (bucket-row blocks, Gram
+    allreduce; world 3 gives uneven blocks) against the reference trajectory."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, kind))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=120)
     assert all(r[1] != "error" for r in res), res
-    with open(os.path.join(GOLDEN, "small_traces.json")) as f:
-        gold = json.load(f)["feasible"]
+    if kind == "gaussian":
+        with open(os.path.join(GOLDEN, "gaussian_traces.json")) as f:
+            gold = json.load(f)["wide"]
+    else:
+        with open(os.path.join(GOLDEN, "small_traces.json")) as f:
+            gold = json.load(f)["feasible"]
     for rank, outer, inner, mu, obj, nx, seeds in res:
         assert outer == gold["outer"] and inner == gold["inner_iterations"]
         assert seeds == [s["sketch_seed"] for s in gold["steps"]]
@@ -75,4 +88,4 @@ def test_sharded_solve_world2_matches_reference():
         # sharded sums change the summation order: same floor as a reordered reference
         assert dev.max() <= 5e-8, dev.max()
         assert abs(obj - gold["objective"]) <= 1e-8 * abs(gold["objective"])
-    assert res[0][3] == res[1][3]  # replicated scalars identical on every rank
+    assert all(r[3] == res[0][3] for r in res)  # replicated scalars identical on every rank
