@@ -130,6 +130,23 @@ def random_feasible_dense(m: int, n: int, density: float, seed: int):
     return A, b, c
 
 
+def random_dense(m: int, n: int, density: float, seed: int):
+    """The reference's random_lp instance (lp_model.py:113-135): same draw
+    order (mask, values, diagonal boost, x0, z, c); b = A x0 + 0.1 z is
+    sign-indefinite against A >= 0, so such draws are infeasible almost surely.
+    Returns dense (A, b, c)."""
+    g = np.random.Generator(np.random.Philox(int(seed)))
+    keep = g.random((m, n)) < density
+    A = np.where(keep, g.random((m, n)), 0.0)
+    k = min(m, n)
+    A[np.arange(k), np.arange(k)] += g.random(k)
+    x0 = g.standard_normal(n)
+    z = g.standard_normal(m)
+    b = A @ x0 + 0.1 * z
+    c = g.standard_normal(n)
+    return A, b, c
+
+
 def ill_conditioned_lp(m: int, n: int, seed: int = 0) -> DenseLP:
     """config c5 with the repaired start of SURVEY.md Appendix C:
     A = diag(r) G, r log-uniform on [1e-3, 1e3]; x0, s0 ~ U(0.5, 1.5)."""
