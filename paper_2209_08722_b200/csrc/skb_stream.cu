@@ -613,10 +613,7 @@ constexpr int kCoopMaxM = 16384;
 static StreamCfg coop_cfg(int m, int64_t n, int64_t lda) {
   StreamCfg c;
   const size_t col_bytes = (size_t)lda * 8;
-  static const size_t cb_bytes = getenv("SKB_COOP_STAGE_KB")
-                                    ? (size_t)atoi(getenv("SKB_COOP_STAGE_KB")) * 1024
-                                    : 32768;
-  c.cb = (int)std::max<size_t>(1, std::min<size_t>(kCoopMaxCb, cb_bytes / col_bytes));
+  c.cb = (int)std::max<size_t>(1, std::min<size_t>(kCoopMaxCb, 32768 / col_bytes));
   const size_t stage_bytes = (size_t)c.cb * col_bytes;
   const size_t head = 256 + 8 * (8 * kCoopMaxCb + kCoopMaxCb * 6) + 128;
   // CTAs per SM: the CTA runs its stages in lockstep, so a second resident CTA
