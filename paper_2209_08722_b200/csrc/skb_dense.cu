@@ -429,31 +429,33 @@ constexpr int NB = 64;
 constexpr int LDP = NB + 1;
 constexpr int kLeafThreads = 256;
 
-// X = L^-1 for the lower 64 x 64 L in Lsm (rinv[q] = 1 / L_qq); this
-// thread's entries X[i][q4 + 4j] come back in x. rowq: 2 x 64 scratch.
-SKB_DEV void leaf_inverse(const double (*Lsm)[LDP], const double* rinv, double (*rowq)[NB],
-                          double (&x)[16]) {
-  const int t = threadIdx.x, i = t >> 2, q4 = t & 3;
+// X = L^-1 for the lower 64 x 64 L in Lsm (rinv[q] = 1 / L_qq) into out (ld).
+SKB_DEV void leaf_inverse(const double (*Lsm)[LDP], const double* rinv, double* out, int64_t ld) {
+  // thread j < 64: column j of L^-1 by right-looking forward substitution, no
+  // barriers; x is rotated every 8 rows (static register indices in a runtime
+  // loop); rows q < j stay zero. out[q * ld + j] stores are coalesced over j.
+  const int j = threadIdx.x;
+  if (j >= NB) return;
+  constexpr int R = 8;
+  double x[NB + R];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) x[j] = (q4 + 4 * j == i) ? 1.0 : 0.0;
-#pragma unroll 2
-  for (int q = 0; q < NB; ++q) {
-    const int buf = q & 1;
-    if (i == q) {
-      const double rq = rinv[q];
+  for (int k = 0; k < NB; ++k) x[k] = (k == j) ? 1.0 : 0.0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        x[j] *= rq;
-        rowq[buf][q4 + 4 * j] = x[j];
-      }
+  for (int k = NB; k < NB + R; ++k) x[k] = 0.0;
+  for (int q0 = 0; q0 < NB; q0 += R) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int q = q0 + u;
+      const double xq = x[u] * rinv[q];
+      out[(int64_t)q * ld + j] = xq;
+      // rows past 63 wrap onto real rows: they only feed discarded entries
+#pragma unroll
+      for (int k = u + 1; k < NB + u; ++k) x[k] = fma(-Lsm[(q0 + k) & (NB - 1)][q], xq, x[k]);
     }
-    __syncthreads();
-    if (i > q) {
-      const double lkq = Lsm[i][q];
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (q4 + 4 * j <= q) x[j] = fma(-lkq, rowq[buf][q4 + 4 * j], x[j]);
-    }
+    for (int k = 0; k < NB; ++k) x[k] = x[k + R];
+#pragma unroll
+    for (int k = NB; k < NB + R; ++k) x[k] = 0.0;
   }
 }
 
@@ -512,45 +514,14 @@ __global__ void __launch_bounds__(kLeafThreads) potrf_diag_kernel(double* G, int
     return;
   }
   if (!Dinv) return;
-  double x[16];
-  leaf_inverse(Lsm, rinv, colc, x);
-#pragma unroll
-  for (int j = 0; j < 16; ++j) Dinv[i * NB + q4 + 4 * j] = x[j];
+  leaf_inverse(Lsm, rinv, Dinv, NB);
 }
 
-// Panel: rows i in [k0+nb, M) of columns [k0, k0+nb): solve x L11' = a by
-// right-looking substitution (the updates of one step are independent).
-__global__ void __launch_bounds__(128) trsm_panel_kernel(double* G, int64_t ld, int k0, int nb,
-                                                          int M) {
-  __shared__ double l[NB][NB + 1];
-  for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-    const int a = t / NB, b = t % NB;
-    l[b][a] = G[(int64_t)(k0 + a) * ld + k0 + b];  // transposed: l[c][q] = L11[q][c]
-  }
-  __syncthreads();
-  const int i = k0 + nb + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  double* row = G + (int64_t)i * ld + k0;
-  double x[NB];
-#pragma unroll
-  for (int c = 0; c < NB; ++c) x[c] = row[c];
-#pragma unroll
-  for (int c = 0; c < NB; ++c) {
-    x[c] = x[c] / l[c][c];
-#pragma unroll
-    for (int q = c + 1; q < NB; ++q) x[q] -= x[c] * l[c][q];
-  }
-#pragma unroll
-  for (int c = 0; c < NB; ++c) row[c] = x[c];
-}
-
-// Inverse of each 64x64 lower-triangular diagonal block: Linv[b] = L[b]^-1.
 // Inverses of the 64 x 64 diagonal blocks of a lower-triangular L (one CTA
 // per block), with the row-parallel scheme of potrf_diag_kernel.
 __global__ void __launch_bounds__(kLeafThreads) trtri_diag_kernel(const double* L, double* Li,
                                                                    int64_t ld) {
   __shared__ double Lsm[NB][LDP];
-  __shared__ double rowq[2][NB];
   __shared__ double rinv[NB];
   const int t = threadIdx.x, i = t >> 2, q4 = t & 3;
   const int64_t b0 = (int64_t)blockIdx.x * NB;
@@ -562,10 +533,7 @@ __global__ void __launch_bounds__(kLeafThreads) trtri_diag_kernel(const double* 
   __syncthreads();
   if (t < NB) rinv[t] = 1.0 / Lsm[t][t];
   __syncthreads();
-  double x[16];
-  leaf_inverse(Lsm, rinv, rowq, x);
-#pragma unroll
-  for (int j = 0; j < 16; ++j) Li[(b0 + i) * ld + b0 + q4 + 4 * j] = x[j];
+  leaf_inverse(Lsm, rinv, Li + b0 * ld + b0, ld);
 }
 
 __global__ void set_identity_pad_kernel(double* G, int64_t ld, int m, int Mp) {
