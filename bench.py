@@ -389,6 +389,15 @@ def run_ours(args):
         except Exception as e:  # report, do not hide
             solve = {"error": f"{type(e).__name__}: {e}"}
 
+    configs = None
+    if world == 1 and not args.no_configs:
+        del lp, op, A, cols, x0, s0, c, d, z, u, zd
+        torch.cuda.empty_cache()
+        try:
+            configs = other_configs(dev)
+        except Exception as e:  # report, do not hide
+            configs = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, det = cpu_sample_normal()
@@ -407,12 +416,120 @@ def run_ours(args):
             "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
             "sketch_precond_build": sketch, "ipm_solve": solve,
+            "other_configs": configs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def _ev_ms(fn, reps, torch):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def other_configs(dev):
+    """Kernel-level numbers of BASELINE configs c3 / c4 / c5 at full size on this
+    GPU (synthetic data of each config's shape in HBM; CUDA events after a
+    warm-up): the fused normal matvec with its algorithmic GB/s, and the sketch
+    + factor build. Full-size time-to-solve of these configs:
+    profiles/r01_solve_c3_c4_c5.jsonl (tools/solve_configs.py)."""
+    import torch
+    from paper_2209_08722_b200 import kernels as K
+    from paper_2209_08722_b200 import preconditioning as PC
+    from paper_2209_08722_b200 import sketching as S
+    from paper_2209_08722_b200.lp_model import DeviceLP
+    from paper_2209_08722_b200.runtime import F64, lda_for
+    out = {}
+    g = torch.Generator(device=dev)
+
+    def build_ms(lp, d, n, w, s, kind):
+        for rep in range(2):  # the first pass warms workspaces and allocations
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            W = (S.build_gaussian_sketch(n, w, 99 + rep) if kind == "gaussian"
+                 else S.build_sparse_embedding(n, w, s, 99 + rep))
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            X = S.apply_sketch(lp, d, W, check_positive=False)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            PC.build_preconditioner(X)
+            torch.cuda.synchronize()
+            t3 = time.perf_counter()
+            del W, X
+        return [round((t1 - t0) * 1e3, 2), round((t2 - t1) * 1e3, 2), round((t3 - t2) * 1e3, 2)]
+
+    # c3: dense m = 2000, n = 4e6 (64 GB)
+    m, n = 2000, 4_000_000
+    g.manual_seed(3)
+    cols = torch.zeros((n, lda_for(m)), dtype=F64, device=dev)
+    cols[:, :m].normal_(generator=g)
+    A = K.DeviceMatrix(cols, m)
+    d2 = torch.rand(n, dtype=F64, device=dev, generator=g) + 0.5
+    z = torch.randn(m, dtype=F64, device=dev, generator=g)
+    u = torch.empty(m, dtype=F64, device=dev)
+    ms = _ev_ms(lambda: K.normal_apply(A, d2, z, u), 5, torch)
+    lp = DeviceLP.from_device(A, torch.zeros(m, dtype=F64, device=dev),
+                              torch.ones(n, dtype=F64, device=dev), n)
+    b = build_ms(lp, d2.sqrt(), n, 8000, 1, "sparse")
+    out["c3"] = {"m": m, "n": n, "matvec_ms": round(ms, 3),
+                 "matvec_GBps": round((8.0 * m * n + 16 * n + 16 * m) / ms / 1e6, 1),
+                 "sketch_w": 8000, "s": 1, "hash_adw_factor_ms": b}
+    del A, cols, lp, d2
+    torch.cuda.empty_cache()
+    # c4: sparse m = 1e4, n = 2e7, 5 nnz / column (CSC)
+    m, n, k = 10_000, 20_000_000, 5
+    g.manual_seed(4)
+    rows = torch.randint(0, m, (n, k), device=dev, generator=g, dtype=torch.int32)
+    rows, _ = torch.sort(rows, dim=1)
+    vals = torch.randn((n, k), dtype=F64, device=dev, generator=g)
+    colptr = torch.arange(0, n * k + 1, k, dtype=torch.int64, device=dev)
+    A = K.SparseDeviceMatrix(colptr, rows.reshape(-1).contiguous(), vals.reshape(-1), m)
+    del rows, vals
+    d2 = torch.rand(n, dtype=F64, device=dev, generator=g) + 0.5
+    z = torch.randn(m, dtype=F64, device=dev, generator=g)
+    u = torch.empty(m, dtype=F64, device=dev)
+    ms = _ev_ms(lambda: K.normal_apply(A, d2, z, u), 5, torch)
+    lp = DeviceLP.from_device(A, torch.zeros(m, dtype=F64, device=dev),
+                              torch.ones(n, dtype=F64, device=dev), n)
+    b = build_ms(lp, d2.sqrt(), n, 40_000, 1, "sparse")
+    nnz = n * k
+    out["c4"] = {"m": m, "n": n, "nnz": nnz, "matvec_ms": round(ms, 3),
+                 "matvec_GBps": round((12.0 * nnz + 16 * n + 16 * m) / ms / 1e6, 1),
+                 "sketch_w": 40_000, "s": 1, "hash_adw_factor_ms": b}
+    del A, lp, d2, colptr
+    torch.cuda.empty_cache()
+    # c5: A = diag(r) G, m = 1000, n = 2e6, dense Gaussian sketch w = 4000
+    m, n, w = 1000, 2_000_000, 4000
+    g.manual_seed(5)
+    cols = torch.zeros((n, lda_for(m)), dtype=F64, device=dev)
+    cols[:, :m].normal_(generator=g)
+    A = K.DeviceMatrix(cols, m)
+    d = torch.rand(n, dtype=F64, device=dev, generator=g) + 0.5
+    z = torch.randn(m, dtype=F64, device=dev, generator=g)
+    u = torch.empty(m, dtype=F64, device=dev)
+    ms = _ev_ms(lambda: K.normal_apply(A, d, z, u), 5, torch)
+    lp = DeviceLP.from_device(A, torch.zeros(m, dtype=F64, device=dev),
+                              torch.ones(n, dtype=F64, device=dev), n)
+    b = build_ms(lp, d, n, w, 0, "gaussian")
+    out["c5"] = {"m": m, "n": n, "matvec_ms": round(ms, 3),
+                 "matvec_GBps": round((8.0 * m * n + 16 * n + 16 * m) / ms / 1e6, 1),
+                 "sketch": "gaussian", "sketch_w": w, "W_gen_adw_gemm_factor_ms": b,
+                 "W_draws_per_s": round(n * w / (b[0] * 1e-3), 1),
+                 "gemm_TFps": round(2.0 * m * n * w / (b[1] * 1e-3) / 1e12, 2)}
+    del A, cols, lp
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -423,6 +540,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the c3/c4/c5 kernel-level numbers (single-GPU runs only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
