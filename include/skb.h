@@ -186,6 +186,15 @@ int skb_sketch_gather(const int32_t* cols, const double* vals, int32_t s, int64_
 size_t skb_gaussian_workspace_bytes(int64_t count);
 int skb_gaussian_sketch(uint64_t key0, uint64_t key1, int64_t lo, int64_t count, int32_t w,
                         double* W, void* workspace, size_t ws_bytes, void* stream);
+
+/* The draws whose ziggurat attempts START in stream positions [p0, p1)
+ * (multiples of 4096), in order, / sqrt(w), into out[0, min(count, cap));
+ * *count_host = count. Consecutive ranges partition the draw sequence
+ * (a rank-parallel W: each rank generates one range, then exchanges by global
+ * draw index). Synchronises the stream. Workspace: skb_gaussian_workspace_bytes. */
+int skb_gaussian_range(uint64_t key0, uint64_t key1, uint64_t p0, uint64_t p1, int32_t w,
+                       double* out, int64_t cap, uint64_t* count_host, void* workspace,
+                       size_t ws_bytes, void* stream);
 int skb_gaussian_apply(const double* A, int64_t m, int64_t n, int64_t lda, const double* d,
                        const double* W, int32_t w, double* X, int64_t ldx, void* workspace,
                        size_t ws_bytes, void* stream);

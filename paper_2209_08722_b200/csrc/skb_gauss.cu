@@ -167,7 +167,8 @@ SKB_DEV uint32_t gs_word(const GaussSmem& S, int r) {
 //  4. block scan of the emitted draws, decoupled look-back for the tile's
 //     global offset, values staged in shared memory and written coalesced.
 __global__ void __launch_bounds__(kZThreads, 3)
-    gauss_onepass_kernel(uint64_t k0, uint64_t k1, uint64_t lo, uint64_t need, double sqrtw,
+    gauss_onepass_kernel(uint64_t k0, uint64_t k1, uint64_t p0, uint64_t lo, uint64_t need,
+                         double sqrtw,
                          double* __restrict__ out, uint64_t* __restrict__ state,
                          uint32_t* __restrict__ ticket, uint32_t tiles, int* __restrict__ err) {
   __shared__ GaussSmem S;
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(kZThreads, 3)
     __syncthreads();
     const uint32_t tile = S.tile;
     if (tile >= tiles) break;
-    const uint64_t t0 = (uint64_t)tile * kZTile;
+    const uint64_t t0 = p0 + (uint64_t)tile * kZTile;  // p0: first position (a tile multiple)
     const uint64_t my0 = t0 + (uint64_t)tid * kZPer;
 
     // ---- 1. classify this thread's words
@@ -487,8 +488,8 @@ extern "C" int skb_gaussian_sketch(uint64_t key0, uint64_t key1, int64_t lo, int
       grid = std::max(1, per) * skb_num_sms();
     }
     gauss_onepass_kernel<<<(unsigned)std::min<uint64_t>(tiles, (uint64_t)grid), kZThreads,
-                           kZTile * 8, st>>>(key0, key1, (uint64_t)lo, (uint64_t)count, sqrtw, W,
-                                             state, ticket, (uint32_t)tiles, err);
+                           kZTile * 8, st>>>(key0, key1, 0, (uint64_t)lo, (uint64_t)count, sqrtw,
+                                             W, state, ticket, (uint32_t)tiles, err);
     uint64_t last = 0;
     int herr = 0;
     cudaMemcpyAsync(&last, state + (tiles - 1), 8, cudaMemcpyDeviceToHost, st);
@@ -500,6 +501,52 @@ extern "C" int skb_gaussian_sketch(uint64_t key0, uint64_t key1, int64_t lo, int
     positions *= 2;
   }
   return SKB_ERR_INTERNAL;
+}
+
+// The draws whose attempts START in stream positions [p0, p1) (multiples of
+// 4096), in stream order, into out[0, count) (count <= cap; *count_host gets
+// the number of draws of the range even when it exceeds cap). Consecutive
+// ranges partition the draw sequence, so ranks can each generate one range
+// and exchange by global draw index (sketching.build_gaussian_sketch).
+// Synchronises the stream.
+extern "C" int skb_gaussian_range(uint64_t key0, uint64_t key1, uint64_t p0, uint64_t p1,
+                                  int32_t w, double* out, int64_t cap, uint64_t* count_host,
+                                  void* workspace, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (w < 1 || cap < 0 || p1 < p0 || (p0 % kZTile) || (p1 % kZTile)) return SKB_ERR_ARG;
+  *count_host = 0;
+  if (p1 == p0) return 0;
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  const double sqrtw = __builtin_sqrt((double)w);
+  const uint64_t tiles = (p1 - p0) / kZTile;
+  if (tiles > 0xffffff00ULL) return SKB_ERR_UNSUPPORTED;
+  uint64_t* state = (uint64_t*)skb_ws_take(&ws, tiles * 8);
+  uint32_t* ticket = (uint32_t*)skb_ws_take(&ws, 16);
+  int* err = (int*)skb_ws_take(&ws, 16);
+  if (!state || !ticket || !err) return SKB_ERR_WORKSPACE;
+  cudaMemsetAsync(state, 0, tiles * 8, st);
+  cudaMemsetAsync(ticket, 0, 16, st);
+  cudaMemsetAsync(err, 0, 16, st);
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(gauss_onepass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kZTile * 8);
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gauss_onepass_kernel, kZThreads,
+                                                  kZTile * 8);
+    grid = std::max(1, per) * skb_num_sms();
+  }
+  gauss_onepass_kernel<<<(unsigned)std::min<uint64_t>(tiles, (uint64_t)grid), kZThreads,
+                         kZTile * 8, st>>>(key0, key1, p0, 0, (uint64_t)cap, sqrtw, out, state,
+                                           ticket, (uint32_t)tiles, err);
+  uint64_t last = 0;
+  int herr = 0;
+  cudaMemcpyAsync(&last, state + (tiles - 1), 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  if (herr) return SKB_ERR_INTERNAL;
+  *count_host = last & kZValMask;
+  return skb_launch_status(__func__);
 }
 
 extern "C" size_t skb_gaussian_workspace_bytes(int64_t count) {

@@ -121,6 +121,33 @@ class Comm:
         dist.all_gather(out, buf, group=self.group)
         return torch.cat(out)[:rows].to(t.device)
 
+    def all_to_all_v(self, t: torch.Tensor, send, recv) -> torch.Tensor:
+        """1-D variable all-to-all: t holds this rank's pieces for ranks
+        0..world-1 back to back (send[h] elements each); returns the pieces
+        received from ranks 0..world-1 back to back (recv[h] each). NCCL
+        all_to_all_single; over gloo every rank gathers every send buffer on
+        the host and cuts its pieces out (tests and CPU runs)."""
+        if self.world == 1:
+            return t
+        if not (self.host_staging or not t.is_cuda):
+            out = torch.empty(sum(recv), dtype=t.dtype, device=t.device)
+            dist.all_to_all_single(out, t, output_split_sizes=list(recv),
+                                   input_split_sizes=list(send), group=self.group)
+            return out
+        sizes = torch.tensor(list(send), dtype=torch.int64)
+        all_sizes = [torch.empty_like(sizes) for _ in range(self.world)]
+        dist.all_gather(all_sizes, sizes, group=self.group)
+        width = max(int(s.sum()) for s in all_sizes)
+        buf = torch.zeros(max(width, 1), dtype=t.dtype)
+        buf[: t.numel()].copy_(t.cpu())
+        bufs = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(bufs, buf, group=self.group)
+        pieces = []
+        for h in range(self.world):
+            off = int(all_sizes[h][: self.rank].sum())
+            pieces.append(bufs[h][off:off + int(all_sizes[h][self.rank])])
+        return torch.cat(pieces).to(t.device)
+
     def barrier(self):
         if self.world > 1:
             dist.barrier(group=self.group)

@@ -120,20 +120,71 @@ def build_identity_sketch(n: int, rows=None) -> SketchOperator:
     return W
 
 
-def build_gaussian_sketch(n: int, w: int, seed: int, rows=None, device=None) -> SketchOperator:
+ZIG_TILE = 4096            # stream positions per generator tile (csrc/skb_gauss.cu)
+ZIG_WORDS_PER_DRAW = 1.0125  # stream words per standard_normal draw, with margin (measured ~1.012)
+
+
+def build_gaussian_sketch(n: int, w: int, seed: int, rows=None, device=None,
+                          comm=None) -> SketchOperator:
     """Dense Gaussian sketch (sketching.py:131-139): standard_normal((n, w)) / sqrt(w)
     drawn on the GPU bit-exact with numpy's ziggurat (K9, csrc/skb_gauss.cu).
-    rows = (j0, j1) keeps this rank's row block (draws j0*w .. j1*w)."""
+    rows = (j0, j1) keeps this rank's row block (draws j0*w .. j1*w). With an
+    active comm every rank generates one slice of the STREAM (not of the draws:
+    draw k's stream position depends on all earlier slow attempts), the per-rank
+    draw counts give each slice's global draw offset, and one all-to-all moves
+    the few draws that landed on a neighbour — no rank walks the whole prefix."""
     if w < 1:
         raise InvalidDims(f"w must be positive, got {w}")
     device = device or require_cuda()
     j0, j1 = rows if rows is not None else (0, n)
     k0, k1 = philox_key(seed)
-    dense = torch.empty((j1 - j0, w), dtype=F64, device=device)
-    need = int(_lib.lib().skb_gaussian_workspace_bytes(j1 * w))
-    ws, cap = workspace(need)
-    _lib.call("skb_gaussian_sketch", k0, k1, j0 * w, j1 * w, w, dense, ws, cap, stream_ptr())
+    if comm is not None and comm.active:
+        dense = _gaussian_rows_distributed(k0, k1, n, w, j0, j1, comm, device)
+    else:
+        dense = torch.empty((j1 - j0, w), dtype=F64, device=device)
+        need = int(_lib.lib().skb_gaussian_workspace_bytes(j1 * w))
+        ws, cap = workspace(need)
+        _lib.call("skb_gaussian_sketch", k0, k1, j0 * w, j1 * w, w, dense, ws, cap, stream_ptr())
     return SketchOperator(kind="gaussian", n=n, w=w, s=0, seed=int(seed), dense=dense, j0=j0)
+
+
+def _gaussian_rows_distributed(k0, k1, n, w, j0, j1, comm, device):
+    from .distributed import shard_range
+    total = n * w
+    ratio = ZIG_WORDS_PER_DRAW
+    for _ in range(4):
+        ptot = -(-int(total * ratio + 8 * ZIG_TILE) // ZIG_TILE) * ZIG_TILE
+        # this rank's stream slice, proportional to its row block
+        p0 = (ptot * j0 // n) // ZIG_TILE * ZIG_TILE
+        p1 = ptot if j1 == n else (ptot * j1 // n) // ZIG_TILE * ZIG_TILE
+        cap = max(1, p1 - p0)  # at most one draw per word
+        buf = torch.empty(cap, dtype=F64, device=device)
+        need = int(_lib.lib().skb_gaussian_workspace_bytes(cap))
+        ws, wcap = workspace(need)
+        cnt = np.zeros(1, dtype=np.uint64)
+        _lib.call("skb_gaussian_range", k0, k1, p0, p1, w, buf, cap, cnt.ctypes.data, ws, wcap,
+                  stream_ptr())
+        counts = comm.allgather_rows(torch.tensor([int(cnt[0])], dtype=torch.int64,
+                                                  device=device), comm.world)
+        counts = [int(c) for c in counts.cpu()]
+        if sum(counts) >= total:
+            break
+        ratio *= 1.01  # too few draws in the stream slices: widen and redo (never observed)
+    else:
+        raise RuntimeError("Gaussian sketch: stream slices never covered n * w draws")
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    mine0, mine1 = int(offs[comm.rank]), int(offs[comm.rank + 1])  # draws this rank holds
+    send, recv = [], []
+    for h in range(comm.world):
+        a0, a1 = shard_range(n, h, comm.world)
+        lo, hi = max(mine0, a0 * w), min(mine1, a1 * w)        # my draws rank h needs
+        send.append(max(0, hi - lo))
+        lo2, hi2 = max(int(offs[h]), j0 * w), min(int(offs[h + 1]), j1 * w)  # h's draws I need
+        recv.append(max(0, hi2 - lo2))
+    a_first = max(mine0, shard_range(n, 0, comm.world)[0] * w)
+    s0 = a_first - mine0
+    out = comm.all_to_all_v(buf[s0:s0 + sum(send)].contiguous(), send, recv)
+    return out.reshape(j1 - j0, w)
 
 
 def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = True):

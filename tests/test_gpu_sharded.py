@@ -89,3 +89,47 @@ def test_sharded_solve_matches_reference(world, kind):
         assert dev.max() <= 5e-8, dev.max()
         assert abs(obj - gold["objective"]) <= 1e-8 * abs(gold["objective"])
     assert all(r[3] == res[0][3] for r in res)  # replicated scalars identical on every rank
+
+
+def _gauss_rank(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2209_08722_b200 import sketching as S
+        from paper_2209_08722_b200.distributed import Comm
+        comm = Comm()
+        n, w = 20_011, 97
+        rows = comm.shard(n)
+        W = S.build_gaussian_sketch(n, w, 4242, rows=rows, comm=comm)
+        q.put((rank, rows, W.dense.cpu().numpy()))
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gaussian_w_stream_slices_bit_exact(world):
+    """Rank-parallel W: each rank generates one slice of the Philox stream,
+    draw offsets from the per-rank counts, one all-to-all for the draws that
+    landed on a neighbour — identical to the single-device W (and to numpy)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    from oracle import ipm_oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_gauss_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+    assert all(r[1] != "error" for r in res), res
+    full = O.gaussian_sketch(20_011, 97, 4242)
+    for rank, (j0, j1), blk in res:
+        assert np.array_equal(blk, full[j0:j1]), rank
