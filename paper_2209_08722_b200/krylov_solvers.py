@@ -9,6 +9,8 @@ host reads the trace once.
 
 from __future__ import annotations
 
+import threading
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -78,14 +80,19 @@ class _PcgBuffers:
         return self.vec[k * self.ldv:k * self.ldv + self.m]
 
 
-_BUF = {}
+# Per-thread (run_comparison runs solves from a thread pool, oracle_bench.py:236):
+# PCG state, trace and host readback buffers are never shared between solves.
+_BUF = threading.local()
 
 
 def _buffers(m: int, t_max: int, device) -> _PcgBuffers:
+    cache = getattr(_BUF, "d", None)
+    if cache is None:
+        cache = _BUF.d = {}
     key = (device.index, m)
-    b = _BUF.get(key)
+    b = cache.get(key)
     if b is None or b.t_cap < t_max:
-        b = _BUF[key] = _PcgBuffers(m, max(t_max, 64), device)
+        b = cache[key] = _PcgBuffers(m, max(t_max, 64), device)
     return b
 
 

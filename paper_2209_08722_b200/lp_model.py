@@ -12,6 +12,7 @@ then `sub` is subtracted.
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -223,17 +224,21 @@ class DeviceLP:
         return math.sqrt(self.vec_stats(a, sub, global_=False)[0])
 
 
-_RED = {}
+_RED = threading.local()
 
 
 def reduction_ws():
-    """Per-device reduction scratch whose ticket word starts (and stays) zero."""
+    """Per-thread, per-device reduction scratch whose ticket word starts (and
+    stays) zero (solves may run from a thread pool, oracle_bench.py:236)."""
+    cache = getattr(_RED, "d", None)
+    if cache is None:
+        cache = _RED.d = {}
     dev = torch.cuda.current_device()
-    buf = _RED.get(dev)
+    buf = cache.get(dev)
     if buf is None:
         nb = int(_lib.lib().skb_reduce_workspace_bytes())
         buf = torch.zeros(nb, dtype=torch.uint8, device=require_cuda())
-        _RED[dev] = buf
+        cache[dev] = buf
     return buf
 
 
