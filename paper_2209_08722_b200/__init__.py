@@ -32,7 +32,14 @@ from .errors import (  # noqa: F401
     Unbounded,
     ZeroRow,
 )
-from .lp_model import DeviceLP, LinearProgram, make_lp, validate  # noqa: F401
+from .lp_model import (  # noqa: F401
+    DeviceLP,
+    LinearProgram,
+    make_lp,
+    random_feasible_lp,
+    random_lp,
+    validate,
+)
 
 __version__ = "0.1.0"
 
@@ -42,6 +49,8 @@ _LAZY = {
     "feasible_start": "ipm_core", "in_neighborhood": "ipm_core", "make_iterate": "ipm_core",
     "phase1_point": "ipm_core", "solve": "ipm_core", "ipm_step": "ipm_core",
     "NormalOperator": "krylov_solvers", "pcg": "krylov_solvers", "SolverTrace": "krylov_solvers",
+    "chebyshev": "krylov_solvers", "direct_solve": "krylov_solvers",
+    "unpreconditioned_cg": "krylov_solvers", "phase1_lp": "start",
     "build_preconditioner": "preconditioning", "apply_inv": "preconditioning",
     "apply_pinv_adw": "preconditioning", "PreconditionerFactor": "preconditioning",
     "SketchOperator": "sketching", "auto_sketch_dims": "sketching",

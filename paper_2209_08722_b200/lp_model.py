@@ -79,6 +79,30 @@ def validate(lp: LinearProgram) -> None:
         raise ZeroRow(int(zero[0]))
 
 
+def random_lp(m: int, n: int, density: float, seed: int) -> LinearProgram:
+    """Reference random_lp (lp_model.py:113-135): same generator and draw order
+    (problems.random_dense); sign-indefinite b, so infeasible almost surely."""
+    from .errors import InvalidDensity
+    from .problems import random_dense
+    if not 0.0 < density <= 1.0:
+        raise InvalidDensity(f"density {density} outside (0, 1]")
+    if n < m:
+        raise DimensionMismatch(f"wide problem required: n={n} < m={m}")
+    A, b, c = random_dense(m, n, density, seed)
+    return make_lp(A, b, c, name=f"random_lp_{m}x{n}_d{density}_s{seed}")
+
+
+def random_feasible_lp(m: int, n: int, density: float, seed: int) -> LinearProgram:
+    """Reference random_feasible_lp (lp_model.py:138-160): strictly feasible primal
+    and dual by construction (problems.random_feasible_dense)."""
+    from .errors import InvalidDensity
+    from .problems import random_feasible_dense
+    if not 0.0 < density <= 1.0:
+        raise InvalidDensity(f"density {density} outside (0, 1]")
+    A, b, c = random_feasible_dense(m, n, density, seed)
+    return make_lp(A, b, c, name=f"random_feasible_lp_{m}x{n}_d{density}_s{seed}")
+
+
 def _dev(a, device):
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=F64).contiguous()

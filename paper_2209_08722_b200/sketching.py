@@ -56,6 +56,21 @@ class SketchOperator:
     def tag(self) -> tuple:
         return (self.kind, self.n, self.w, self.s, self.seed)
 
+    def as_sparse(self):
+        """W (this rank's rows) as a host scipy CSR matrix with sorted column
+        indices (sketching.py:53-69); identity and sparse-sign sketches only."""
+        import scipy.sparse as sp
+        if self.kind == "identity":
+            return sp.identity(self.n, format="csr")[self.j0:self.j0 + self.n_local]
+        if self.kind != "sparse_sign":
+            raise DimensionMismatch("as_sparse only applies to sparse_sign sketches")
+        rows = self.n_local
+        csr = sp.csr_matrix((self.vals.cpu().numpy().ravel().copy(),
+                             self.cols.cpu().numpy().ravel().astype(np.int64),
+                             np.arange(0, rows * self.s + 1, self.s)), shape=(rows, self.w))
+        csr.sort_indices()
+        return csr
+
     def matvec(self, u: torch.Tensor) -> torch.Tensor:
         """W u for a length-w device vector (local rows)."""
         if u.shape != (self.w,):

@@ -73,6 +73,21 @@ def test_sparse_embedding_rows(dev, n, w, s, seed):
     assert np.allclose(_h(W.matvec(_t(u))), D @ u, atol=1e-14)
 
 
+def test_as_sparse_matches_reference_layout(dev):
+    from paper_2209_08722_b200 import sketching as S
+    from paper_2209_08722_b200.errors import DimensionMismatch
+    W = S.build_sparse_embedding(50, 24, 3, 9)
+    csr = W.as_sparse()
+    cols, vals = O.sparse_embedding(50, 24, 3, 9)
+    D = np.zeros((50, 24))
+    for j in range(50):
+        D[j, cols[j]] = vals[j]
+    assert np.array_equal(csr.toarray(), D) and csr.has_sorted_indices
+    assert np.array_equal(S.build_identity_sketch(4).as_sparse().toarray(), np.eye(4))
+    with pytest.raises(DimensionMismatch):
+        S.build_gaussian_sketch(10, 3, 1).as_sparse()
+
+
 def test_sketch_invalid_dims(dev):
     from paper_2209_08722_b200 import sketching as S
     from paper_2209_08722_b200.errors import InvalidDims

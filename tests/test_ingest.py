@@ -155,3 +155,21 @@ def test_null_pair_columns():
     A = np.stack([a, -a, -a, a, a, 2 * a, np.array([0.0, 0.0, 1.0])], axis=1)
     c = np.array([0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0])
     assert _null_pair_columns(LinearProgram(sp.csr_matrix(A), np.ones(3), c)) == [(0, 1), (2, 3)]
+
+
+def test_reference_generators_identical():
+    """random_lp / random_feasible_lp reproduce the reference's instances
+    (tests/golden/start_traces.json pins random_feasible_lp(20, 200, 0.5, 3))."""
+    from paper_2209_08722_b200 import random_feasible_lp, random_lp
+    from paper_2209_08722_b200.errors import DimensionMismatch, InvalidDensity
+    lp = random_feasible_lp(20, 200, 0.5, 3)
+    assert lp.name == "random_feasible_lp_20x200_d0.5_s3" and lp.A.shape == (20, 200)
+    with open(os.path.join(GOLDEN, "start_traces.json")) as f:
+        gold = json.load(f)
+    x0 = np.array(gold["phase1_x0"])            # A x0 = b for the reference's instance
+    assert np.linalg.norm(lp.A @ x0 - lp.b) <= 1e-6 * np.linalg.norm(lp.b)
+    with pytest.raises(InvalidDensity):
+        random_lp(3, 5, 0.0, 1)
+    with pytest.raises(DimensionMismatch):
+        random_lp(5, 3, 0.5, 1)
+    assert random_lp(4, 9, 0.5, 2).name == "random_lp_4x9_d0.5_s2"
