@@ -10,18 +10,24 @@
 // (two uniforms per round). Attempt lengths vary, so draw k's position
 // depends on every earlier slow attempt: a sequential recurrence.
 //
-// B200 mapping (one pass, persistent CTAs, tiles of 4096 positions taken in
-// ticket order): each thread draws and classifies 16 words; the rare slow
-// attempts (~1.2%) are listed in position order and evaluated by the whole
-// CTA in parallel; their chaining (which listed words start attempts) needs
-// only integer work from an anchor — the latest position preceded by 64 fast
-// words, found in a backward halo — and is resolved per run between "sync
-// points". The tile's draw count feeds a decoupled look-back that gives its
-// global offset; values are staged in shared memory and stored coalesced.
+// B200 mapping: four kernels over tiles of 4096 stream positions, every one
+// of them parallel across tiles (no tile waits on another):
+//  K9a classify: Philox + the fast test for every word -> a 1-bit-per-word
+//      "slow" bitmap (1/8 byte per draw), no barriers;
+//  K9b chain (one warp per tile): anchor = the latest position before the
+//      tile preceded by 64 fast words (read from the bitmap), the tile's slow
+//      positions listed in order, their attempts evaluated by the lanes, and
+//      chained between "sync points" into consumed / accepted bitmaps and the
+//      tile's draw count;
+//  K9c exclusive scan of the counts (CUB) -> each tile's first draw index;
+//  K9d emit: Philox again, fast values, accepted slow values recomputed,
+//      block ranks, staged in shared memory and stored coalesced.
 // The tables come from numpy's own build (ziggurat_tables.py -> generated
-// header) and are copied to shared memory (random per-lane index).
+// header) and live in shared memory (random per-lane index).
 #include <algorithm>
 #include <climits>
+
+#include <cub/device/device_scan.cuh>
 
 #include "skb_common.cuh"
 #include "skb_internal.h"
@@ -121,334 +127,320 @@ SKB_DEV double div_by(double x, double c, double rc) {
   return __fma_rn(r, rc, q);
 }
 
-// Tile state words for the decoupled look-back: flag in bits 62-63.
-constexpr uint64_t kZFlagAgg = 1ULL << 62;   // tile's own draw count published
-constexpr uint64_t kZFlagIncl = 2ULL << 62;  // inclusive prefix published
-constexpr uint64_t kZValMask = (1ULL << 62) - 1;
-constexpr int kZHalo = 256;       // positions per backward halo chunk (64 Philox blocks)
-constexpr int kZHaloChunks = 16;  // anchor search depth (4096 positions)
-constexpr int kZListMax = 192;    // slow positions per tile + halo (mean ~30)
+constexpr int kZHaloTiles = 4;           // anchor search depth before a range start
+constexpr int kZWords = kZTile / 32;     // bitmap words per tile
+constexpr int kZListMax = 512;           // listed slow positions per tile (mean ~50)
+constexpr int kZChainWarps = 4;
 
-struct GaussSmem {
-  ZigTables T;
-  uint32_t slow_bits[kZTile / 32];  // tile positions whose word fails the fast test
-  uint32_t skip_bits[kZTile / 32];  // consumed by a slow attempt
-  uint32_t acc_bits[kZTile / 32];   // accepted slow attempt starts
-  uint32_t halo_w[kZHalo * kZHaloChunks / 32];  // halo_w[k]: [t0-32(k+1), t0-32k)
-  int32_t l_off[kZListMax];         // slow positions from the anchor on, ascending (rel. t0)
-  int32_t l_pm[kZListMax];          // prefix max of earlier attempt ends (chain bound)
-  double l_val[kZListMax];
-  uint8_t l_len[kZListMax];
-  uint8_t l_ok[kZListMax];
-  uint32_t warp_sum[kZThreads / 32];
-  uint64_t prefix;
-  uint32_t tile;
-  int32_t anchor;  // relative to t0 (<= 0)
-  int list_n;
-  int anchored;
-};
-
-// Slow-bit word at relative word index r (r >= 0: tile, r < 0: halo).
-SKB_DEV uint32_t gs_word(const GaussSmem& S, int r) {
-  return r >= 0 ? S.slow_bits[r] : S.halo_w[-r - 1];
-}
-
-// Persistent kernel; each CTA takes tiles of positions [t0, t0 + 4096) in
-// ticket order, so the look-back only ever waits on running/finished tiles:
-//  1. every thread draws its 16 words (4 Philox blocks), keeps their fast
-//     values in registers and flags the slow ones (~0.7%) in a bitmap;
-//  2. backward halo chunks of 256 positions until the anchor is found: the
-//     latest a <= t0 preceded by 64 fast words (an attempt start whenever
-//     every attempt is <= 64 words, which the chain checks);
-//  3. warp 0 compacts the slow positions in [a, t0 + 4096) into an ascending
-//     list; the whole CTA evaluates those attempts in parallel (value,
-//     accept, length); one lane chains them with the stored lengths and
-//     marks the consumed words;
-//  4. block scan of the emitted draws, decoupled look-back for the tile's
-//     global offset, values staged in shared memory and written coalesced.
-__global__ void __launch_bounds__(kZThreads, 3)
-    gauss_onepass_kernel(uint64_t k0, uint64_t k1, uint64_t p0, uint64_t lo, uint64_t need,
-                         double sqrtw,
-                         double* __restrict__ out, uint64_t* __restrict__ state,
-                         uint32_t* __restrict__ ticket, uint32_t tiles, int* __restrict__ err) {
-  __shared__ GaussSmem S;
-  extern __shared__ double stage[];  // kZTile outputs by rank (dynamic: 32 KB)
-  const double rsqrtw = __drcp_rn(sqrtw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  zig_load_tables(&S.T);
-  for (;;) {
-    if (tid == 0) S.tile = atomicAdd(ticket, 1u);
-    if (tid < kZTile / 32) {
-      S.skip_bits[tid] = 0;
-      S.acc_bits[tid] = 0;
-    }
-    __syncthreads();
-    const uint32_t tile = S.tile;
-    if (tile >= tiles) break;
-    const uint64_t t0 = p0 + (uint64_t)tile * kZTile;  // p0: first position (a tile multiple)
-    const uint64_t my0 = t0 + (uint64_t)tid * kZPer;
-
-    // ---- 1. classify this thread's words
-    double vv[kZPer];
+// ---- K9a: slow bitmap of positions [base, base + 32 * nwords)
+__global__ void __launch_bounds__(256)
+    zig_classify_kernel(uint64_t k0, uint64_t k1, uint64_t base, int64_t nwords,
+                        uint32_t* __restrict__ bits) {
+  __shared__ uint64_t ki[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) ki[i] = zig_ki_double_bits[i];
+  __syncthreads();
+  for (int64_t wd = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wd < nwords;
+       wd += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = base + 32 * (uint64_t)wd;
     uint32_t mask = 0;
 #pragma unroll
-    for (int b = 0; b < kZPer / 4; ++b) {
-      const u64x4 o = philox4x64_10(((my0 >> 2) + b) + 1, 0, 0, 0, k0, k1);
+    for (int b = 0; b < 8; ++b) {
+      const u64x4 o = philox4x64_10(((p >> 2) + b) + 1, 0, 0, 0, k0, k1);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        vv[4 * b + i] = zig_fast_value(S.T, o.v[i]);
-        if (!zig_fast(S.T, o.v[i])) mask |= 1u << (4 * b + i);
+        const uint64_t r = o.v[i];
+        const uint64_t rabs = (r >> 9) & 0x000fffffffffffffULL;
+        if (!(rabs < ki[r & 0xff])) mask |= 1u << (4 * b + i);
       }
     }
-    {
-      const uint32_t other = __shfl_xor_sync(0xffffffffu, mask, 1);
-      if ((tid & 1) == 0) S.slow_bits[tid >> 1] = mask | (other << 16);
-    }
-    if (tid == 0) {
-      S.anchored = (t0 == 0);
-      S.anchor = 0;
-    }
-    __syncthreads();
+    bits[wd] = mask;
+  }
+}
 
-    // ---- 2. anchor from backward halo chunks
-    int32_t a_rel = 0;  // thread 0: current candidate (relative to t0)
-    int chunks = 0;
-    while (!S.anchored) {
-      const int c = chunks;
-      if (c == kZHaloChunks) {
-        if (tid == 0) atomicOr(err, 2);  // (never observed: 4096 words without a 64-run)
-        break;
-      }
-      if (tid < 8) S.halo_w[8 * c + tid] = 0;
-      __syncthreads();
-      if (tid < kZHalo / 4) {
-        const int64_t p0 = (int64_t)t0 - (int64_t)kZHalo * (c + 1) + 4 * tid;
-        if (p0 >= 0) {
-          const u64x4 o = philox4x64_10(((uint64_t)p0 >> 2) + 1, 0, 0, 0, k0, k1);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (!zig_fast(S.T, o.v[i])) {
-              const int dd = kZHalo * (c + 1) - 4 * tid - i;  // t0 - p, in [1, 256 (c+1)]
-              const int k = (dd - 1) >> 5;
-              atomicOr(&S.halo_w[k], 1u << (32 * (k + 1) - dd));
-            }
-          }
-        }
-      }
-      __syncthreads();
-      ++chunks;
-      if (tid == 0) {
-        // lowest relative position covered (clipped at the stream start)
-        const int32_t low = (int64_t)t0 - (int64_t)kZHalo * chunks < 0 ? -(int32_t)t0
-                                                                       : -kZHalo * chunks;
-        for (;;) {
-          // highest slow position s in [low, a_rel)
-          int32_t s = INT32_MIN;
-          for (int32_t q = a_rel - 1; q >= low;) {
-            const int r = q >> 5;  // floor division (arithmetic shift)
-            uint32_t wbits = gs_word(S, r) & (0xffffffffu >> (31 - (q & 31)));
-            if (wbits) {
-              s = r * 32 + (31 - __clz(wbits));
-              break;
-            }
-            q = r * 32 - 1;
-          }
-          if (s == INT32_MIN) {
-            if (a_rel - low >= kZMaxLen || low == -(int32_t)t0) {
-              S.anchor = a_rel;
-              S.anchored = 1;
-            }
-            break;  // else: need another chunk
-          }
-          if (a_rel - s > kZMaxLen) {
-            S.anchor = a_rel;
-            S.anchored = 1;
+struct ZigChainWarp {
+  int32_t off[kZListMax];   // slow positions from the anchor on, ascending (relative t0)
+  int32_t pm[kZListMax];    // prefix max of earlier attempt ends
+  uint8_t len[kZListMax];
+  uint8_t ok[kZListMax];
+  uint32_t skip[kZWords];
+  uint32_t acc[kZWords];
+};
+
+// ---- K9b: one warp per tile; bits cover positions [base, ...) with base <= P0 - halo
+__global__ void __launch_bounds__(32 * kZChainWarps)
+    zig_chain_kernel(uint64_t k0, uint64_t k1, uint64_t P0, uint64_t base,
+                     const uint32_t* __restrict__ bits, int64_t tiles,
+                     uint32_t* __restrict__ gskip, uint32_t* __restrict__ gacc,
+                     uint64_t* __restrict__ cnt, int* __restrict__ err) {
+  __shared__ ZigTables T;
+  __shared__ ZigChainWarp W[kZChainWarps];
+  zig_load_tables(&T);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  ZigChainWarp& S = W[wl];
+  for (int64_t tile = (int64_t)blockIdx.x * kZChainWarps + wl; tile < tiles;
+       tile += (int64_t)gridDim.x * kZChainWarps) {
+    const uint64_t t0 = P0 + (uint64_t)tile * kZTile;
+    const int64_t r_t0 = (int64_t)((t0 - base) / 32);  // bitmap word of t0
+    auto word = [&](int64_t r_rel) -> uint32_t {       // word at relative index (t0 = 0)
+      const int64_t g = r_t0 + r_rel;
+      return g >= 0 ? bits[g] : 0u;
+    };
+    for (int q = lane; q < kZWords; q += 32) {
+      S.skip[q] = 0;
+      S.acc[q] = 0;
+    }
+    // anchor (lane 0): latest a <= 0 with 64 fast predecessors, or the stream start
+    int32_t anc = 0;
+    if (lane == 0 && t0 > 0) {
+      const int32_t low = -(int32_t)(t0 - base);  // lowest position with known bits
+      int32_t a = 0;
+      bool found = false;
+      for (;;) {
+        int32_t sl = INT32_MIN;
+        for (int32_t q = a - 1; q >= low;) {
+          const int32_t r = q >> 5;
+          const uint32_t wbits = word(r) & (0xffffffffu >> (31 - (q & 31)));
+          if (wbits) {
+            sl = r * 32 + (31 - __clz(wbits));
             break;
           }
-          a_rel = s;
+          q = r * 32 - 1;
         }
+        if (sl == INT32_MIN) {
+          found = (a - low >= kZMaxLen) || base == 0;  // ... or fast back to the stream start
+          break;
+        }
+        if (a - sl > kZMaxLen) {
+          found = true;
+          break;
+        }
+        a = sl;
       }
-      __syncthreads();
+      if (!found) atomicOr(err, 2);  // (never observed: 16K words without a 64-run)
+      anc = a;
     }
-
-    // ---- 3a. ascending list of slow positions in [anchor, t0 + 4096)
-    if (warp == 0) {
-      const int32_t anc = S.anchor;
-      const int r_lo = anc >> 5;  // floor
-      const int nw = kZTile / 32 - r_lo;
+    anc = __shfl_sync(0xffffffffu, anc, 0);
+    // ascending list of slow positions in [anc, 4096)
+    {
+      const int r_lo = anc >> 5;
+      const int nw = kZWords - r_lo;
       const int per = (nw + 31) / 32;
       const int rb = r_lo + lane * per;
-      int cnt = 0;
+      int c = 0;
       for (int t = 0; t < per; ++t) {
         const int r = rb + t;
-        if (r >= kZTile / 32) break;
-        uint32_t wbits = gs_word(S, r);
+        if (r >= kZWords) break;
+        uint32_t wbits = word(r);
         if (r * 32 < anc) wbits &= 0xffffffffu << (anc - r * 32);
-        cnt += __popc(wbits);
+        c += __popc(wbits);
       }
-      int incl = cnt;
+      int incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += t;
       }
-      int pos = incl - cnt;
+      int pos = incl - c;
       for (int t = 0; t < per; ++t) {
         const int r = rb + t;
-        if (r >= kZTile / 32) break;
-        uint32_t wbits = gs_word(S, r);
+        if (r >= kZWords) break;
+        uint32_t wbits = word(r);
         if (r * 32 < anc) wbits &= 0xffffffffu << (anc - r * 32);
         while (wbits) {
           const int b = __ffs(wbits) - 1;
           wbits &= wbits - 1;
-          if (pos < kZListMax) S.l_off[pos] = r * 32 + b;
+          if (pos < kZListMax) S.off[pos] = r * 32 + b;
           ++pos;
         }
       }
-      if (lane == 31) {
-        S.list_n = min(incl, kZListMax);
-        if (incl > kZListMax) atomicOr(err, 4);
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 0 && total > kZListMax) atomicOr(err, 4);
+      __syncwarp();
+      const int nlist = min(total, kZListMax);
+      // evaluate every listed attempt (lanes in parallel)
+      for (int i = lane; i < nlist; i += 32) {
+        const uint64_t q = (uint64_t)((int64_t)t0 + S.off[i]);
+        double v;
+        int len;
+        const bool ok = zig_slow(T, k0, k1, q, out64(k0, k1, q), &v, &len);
+        S.len[i] = (uint8_t)min(len, 255);
+        S.ok[i] = ok;
       }
-    }
-    __syncthreads();
-    // ---- 3b. evaluate every listed attempt in parallel
-    const int nlist = S.list_n;
-    for (int i = tid; i < nlist; i += kZThreads) {
-      const uint64_t q = (uint64_t)((int64_t)t0 + S.l_off[i]);
-      double v = 0.0;
-      int len;
-      const bool ok = zig_slow(S.T, k0, k1, q, out64(k0, k1, q), &v, &len);
-      S.l_val[i] = v;
-      S.l_len[i] = (uint8_t)min(len, 255);
-      S.l_ok[i] = ok;
-    }
-    __syncthreads();
-    // ---- 3c. chain. PM_i = max(anchor, ends of all earlier entries as if
-    // every entry were an attempt) bounds the true next free word, so an
-    // entry with off_i >= PM_i is certainly an attempt (a sync point). Each
-    // lane owning a sync point resolves, in order, the entries up to the
-    // next sync point (short runs: only adjacent slow words conflict).
-    if (warp == 0) {
-      int32_t carry = S.anchor;
+      __syncwarp();
+      // prefix max of attempt ends (as if every entry were an attempt)
+      int32_t carry = anc;
       for (int b = 0; b < nlist; b += 32) {
         const int i = b + lane;
         const bool valid = i < nlist;
-        const int32_t e = valid ? S.l_off[i] + (int32_t)S.l_len[i] : INT32_MIN;
-        int32_t pm = e;
+        const int32_t e = valid ? S.off[i] + (int32_t)S.len[i] : INT32_MIN;
+        int32_t pmv = e;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const int32_t t = __shfl_up_sync(0xffffffffu, pm, o);
-          if (lane >= o) pm = max(pm, t);
+          const int32_t t = __shfl_up_sync(0xffffffffu, pmv, o);
+          if (lane >= o) pmv = max(pmv, t);
         }
-        int32_t before = __shfl_up_sync(0xffffffffu, pm, 1);
+        int32_t before = __shfl_up_sync(0xffffffffu, pmv, 1);
         before = lane == 0 ? carry : max(before, carry);
-        if (valid) S.l_pm[i] = before;
-        carry = max(carry, __shfl_sync(0xffffffffu, pm, 31));
+        if (valid) S.pm[i] = before;
+        carry = max(carry, __shfl_sync(0xffffffffu, pmv, 31));
       }
       __syncwarp();
+      // chain between sync points
       for (int i = lane; i < nlist; i += 32) {
-        if (S.l_off[i] < S.l_pm[i]) continue;  // not a sync point
+        if (S.off[i] < S.pm[i]) continue;
         int32_t next_free = INT32_MIN;
-        for (int k = i; k < nlist && (k == i || S.l_off[k] < S.l_pm[k]); ++k) {
-          const int32_t so = S.l_off[k];
-          if (so < next_free) continue;  // consumed by the previous attempt
-          const int len = S.l_len[k];
+        for (int k = i; k < nlist && (k == i || S.off[k] < S.pm[k]); ++k) {
+          const int32_t so = S.off[k];
+          if (so < next_free) continue;
+          const int len = S.len[k];
           if (len > kZMaxLen) atomicOr(err, 1);
-          if (so >= 0 && S.l_ok[k]) atomicOr(&S.acc_bits[so >> 5], 1u << (so & 31));
+          if (so >= 0 && S.ok[k]) atomicOr(&S.acc[so >> 5], 1u << (so & 31));
           const int32_t e = min(so + len, kZTile);
-          for (int32_t p = max(so + 1, 0); p < e;) {  // consumed words in the tile
+          for (int32_t p = max(so + 1, 0); p < e;) {
             const int r = p >> 5, b0 = p & 31;
             const int nb = min(32 - b0, e - p);
-            atomicOr(&S.skip_bits[r], (nb == 32 ? 0xffffffffu : ((1u << nb) - 1u)) << b0);
+            atomicOr(&S.skip[r], (nb == 32 ? 0xffffffffu : ((1u << nb) - 1u)) << b0);
             p += nb;
           }
           next_free = so + len;
         }
       }
+      __syncwarp();
     }
-    __syncthreads();
+    // the tile's draws: visited fast words + accepted slow attempts
+    uint64_t c = 0;
+    for (int q = lane; q < kZWords; q += 32) {
+      const uint32_t sk = S.skip[q], ac = S.acc[q];
+      c += __popc((~word(q) & ~sk) | ac);
+      gskip[tile * kZWords + q] = sk;
+      gacc[tile * kZWords + q] = ac;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[tile] = c;
+    __syncwarp();
+  }
+}
 
-    // ---- 4. scan, look-back, staged coalesced store
-    const uint32_t sk = (S.skip_bits[tid >> 1] >> ((tid & 1) * 16)) & 0xffffu;
-    const uint32_t ac = (S.acc_bits[tid >> 1] >> ((tid & 1) * 16)) & 0xffffu;
-    const uint32_t outm = ((~mask & 0xffffu) & ~sk) | ac;  // visited fast | accepted slow
-    const uint32_t cnt = __popc(outm);
-    uint32_t incl = cnt;
+// ---- K9d: emit the tile's draws at their global indices (offs: exclusive scan).
+// Each thread's draws are consecutive in the output (its rank range), so
+// they are stored directly (no staging barrier); the warp's ranges abut.
+__global__ void __launch_bounds__(kZThreads, 3)
+    zig_emit_kernel(uint64_t k0, uint64_t k1, uint64_t P0, int64_t tiles,
+                    const uint32_t* __restrict__ gskip, const uint32_t* __restrict__ gacc,
+                    const uint64_t* __restrict__ offs, uint64_t lo, uint64_t need,
+                    double sqrtw, double* __restrict__ out) {
+  __shared__ ZigTables T;
+  __shared__ uint32_t warp_sum[2][kZThreads / 32];
+  zig_load_tables(&T);
+  const double rsqrtw = __drcp_rn(sqrtw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __syncthreads();
+  int par = 0;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, par ^= 1) {
+    const uint64_t t0 = P0 + (uint64_t)tile * kZTile;
+    const uint64_t my0 = t0 + (uint64_t)tid * kZPer;
+    const uint64_t base = offs[tile];
+    const uint64_t tcount = offs[tile + 1] - base;
+    if (base >= need || base + tcount <= lo) continue;  // uniform across the CTA
+    const uint32_t sk = (gskip[tile * kZWords + (tid >> 1)] >> ((tid & 1) * 16)) & 0xffffu;
+    const uint32_t ac = (gacc[tile * kZWords + (tid >> 1)] >> ((tid & 1) * 16)) & 0xffffu;
+    double vv[kZPer];
+    uint32_t slow = 0;
+#pragma unroll
+    for (int b = 0; b < kZPer / 4; ++b) {
+      const u64x4 o = philox4x64_10(((my0 >> 2) + b) + 1, 0, 0, 0, k0, k1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        vv[4 * b + i] = zig_fast_value(T, o.v[i]);
+        if (!zig_fast(T, o.v[i])) slow |= 1u << (4 * b + i);
+      }
+    }
+    const uint32_t outm = ((~slow & 0xffffu) & ~sk) | ac;
+    const uint32_t c = __popc(outm);
+    uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    if (lane == 31) S.warp_sum[warp] = incl;
-    if (ac) {  // accepted slow values from the list (binary search; rare)
-#pragma unroll
-      for (int i = 0; i < kZPer; ++i) {
-        if (ac & (1u << i)) {
-          const int32_t off = tid * kZPer + i;
-          int lo_i = 0, hi_i = nlist - 1;
-          while (lo_i < hi_i) {
-            const int mid = (lo_i + hi_i) >> 1;
-            if (S.l_off[mid] < off) lo_i = mid + 1;
-            else hi_i = mid;
-          }
-          vv[i] = S.l_val[lo_i];
-        }
-      }
-    }
+    if (lane == 31) warp_sum[par][warp] = incl;  // double-buffered: one barrier per tile
     __syncthreads();
-    uint32_t wbase = 0, total = 0;
+    uint32_t wbase = 0;
 #pragma unroll
-    for (int w2 = 0; w2 < kZThreads / 32; ++w2) {
-      const uint32_t t = S.warp_sum[w2];
-      if (w2 < warp) wbase += t;
-      total += t;
-    }
-    const uint32_t excl = wbase + incl - cnt;
+    for (int w2 = 0; w2 < kZThreads / 32; ++w2)
+      if (w2 < warp) wbase += warp_sum[par][w2];
+    const uint64_t first = base + wbase + incl - c;  // global index of this thread's first draw
 #pragma unroll
     for (int i = 0, k = 0; i < kZPer; ++i) {
       if (outm & (1u << i)) {
-        stage[excl + k] = div_by(vv[i], sqrtw, rsqrtw);
+        const uint64_t idx = first + k;
+        if (!((ac >> i) & 1u) && idx >= lo && idx < need)
+          out[idx - lo] = div_by(vv[i], sqrtw, rsqrtw);
         ++k;
       }
     }
-    if (warp == 0) {
-      volatile uint64_t* vs = state;
-      if (lane == 0)
-        vs[tile] = (tile == 0 ? uint64_t(kZFlagIncl) : uint64_t(kZFlagAgg)) | (uint64_t)total;
-      uint64_t prefix = 0;
-      int64_t j = (int64_t)tile - 1;
-      while (j >= 0) {
-        const int64_t idx = j - lane;
-        uint64_t sv = idx >= 0 ? uint64_t(vs[idx]) : uint64_t(kZFlagIncl);
-        int first;
-        for (;;) {
-          const uint32_t ready = __ballot_sync(0xffffffffu, (sv >> 62) != 0);
-          const uint32_t incl_m = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
-          first = incl_m ? __ffs(incl_m) - 1 : 32;
-          const uint32_t need_m = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
-          if ((ready & need_m) == need_m) break;
-          if ((sv >> 62) == 0) sv = vs[idx];
-        }
-        uint64_t part = (lane <= first && idx >= 0) ? (sv & kZValMask) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        prefix += part;
-        if (first < 32) break;
-        j -= 32;
-      }
-      if (lane == 0) {
-        if (tile > 0) vs[tile] = kZFlagIncl | (prefix + total);
-        S.prefix = prefix;
-      }
+    // accepted slow attempts (rare): recompute their values in a rolled loop
+    for (uint32_t rest = ac; rest; rest &= rest - 1) {
+      const int i = __ffs(rest) - 1;
+      const uint64_t idx = first + __popc(outm & ((1u << i) - 1u));
+      if (idx < lo || idx >= need) continue;
+      const uint64_t q = my0 + i;
+      double v;
+      int len;
+      zig_slow(T, k0, k1, q, out64(k0, k1, q), &v, &len);
+      out[idx - lo] = div_by(v, sqrtw, rsqrtw);
     }
-    __syncthreads();
-    const uint64_t base = S.prefix;
-    for (uint32_t k = tid; k < total; k += kZThreads) {
-      const uint64_t idx = base + k;
-      if (idx >= lo && idx < need) out[idx - lo] = stage[k];
-    }
-    __syncthreads();
   }
+}
+
+// Draws of the stream positions [P0, P1) (tile multiples), written as
+// out[idx - lo] for global draw indices lo <= idx < need (idx counted from the
+// first attempt starting at or after P0). *total = draws of the range.
+static int zig_generate(uint64_t k0, uint64_t k1, uint64_t P0, uint64_t P1, uint64_t lo,
+                        uint64_t need, int32_t w, double* out, uint64_t* total, skb_ws* ws,
+                        cudaStream_t st) {
+  const int64_t tiles = (int64_t)((P1 - P0) / kZTile);
+  *total = 0;
+  if (tiles <= 0) return 0;
+  const uint64_t base = P0 >= (uint64_t)kZHaloTiles * kZTile ? P0 - kZHaloTiles * kZTile : 0;
+  const int64_t nwords = (int64_t)((P1 - base) / 32);
+  uint32_t* bits = (uint32_t*)skb_ws_take(ws, (size_t)nwords * 4);
+  uint32_t* gskip = (uint32_t*)skb_ws_take(ws, (size_t)tiles * kZWords * 4);
+  uint32_t* gacc = (uint32_t*)skb_ws_take(ws, (size_t)tiles * kZWords * 4);
+  uint64_t* cnt = (uint64_t*)skb_ws_take(ws, (size_t)(tiles + 1) * 8);
+  uint64_t* offs = (uint64_t*)skb_ws_take(ws, (size_t)(tiles + 1) * 8);
+  int* err = (int*)skb_ws_take(ws, 16);
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, offs, (int)(tiles + 1), st);
+  void* scan_tmp = skb_ws_take(ws, scan_bytes + 16);
+  if (!bits || !gskip || !gacc || !cnt || !offs || !err || !scan_tmp) return SKB_ERR_WORKSPACE;
+  if (tiles + 1 > 0x7fffffffLL) return SKB_ERR_UNSUPPORTED;
+  cudaMemsetAsync(err, 0, 16, st);
+  cudaMemsetAsync(cnt + tiles, 0, 8, st);
+  const int sms = skb_num_sms();
+  zig_classify_kernel<<<(unsigned)std::min<int64_t>((nwords + 255) / 256, 64LL * sms), 256, 0,
+                        st>>>(k0, k1, base, nwords, bits);
+  zig_chain_kernel<<<(unsigned)std::min<int64_t>((tiles + kZChainWarps - 1) / kZChainWarps,
+                                                 16LL * sms),
+                     32 * kZChainWarps, 0, st>>>(k0, k1, P0, base, bits, tiles, gskip, gacc, cnt,
+                                                 err);
+  cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, offs, (int)(tiles + 1), st);
+  if (need > lo)
+    zig_emit_kernel<<<(unsigned)std::min<int64_t>(tiles, 8LL * sms), kZThreads, 0, st>>>(
+        k0, k1, P0, tiles, gskip, gacc, offs, lo, need, __builtin_sqrt((double)w), out);
+  int herr = 0;
+  cudaMemcpyAsync(total, offs + tiles, 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  if (herr) return SKB_ERR_INTERNAL;  // an attempt longer than 64 words (never observed)
+  return skb_launch_status("zig_generate");
+}
+
+static uint64_t zig_positions_for(uint64_t count) {
+  const uint64_t p = count + count / 64 + 4 * (uint64_t)kZTile;
+  return (p + kZTile - 1) / kZTile * kZTile;
 }
 
 }  // namespace skb
@@ -457,48 +449,22 @@ using namespace skb;
 
 // W = draws [lo, count) of standard_normal / sqrt(w) (row-major n x w when
 // lo = 0, count = n*w; a rank's row block with lo = j0*w, count = j1*w).
-// Synchronises the stream (tile count check).
+// Synchronises the stream.
 extern "C" int skb_gaussian_sketch(uint64_t key0, uint64_t key1, int64_t lo, int64_t count,
                                    int32_t w, double* W, void* workspace, size_t ws_bytes,
                                    void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (count < 0 || lo < 0 || lo > count || w < 1) return SKB_ERR_ARG;
   if (count == lo) return 0;
-  skb_ws ws = skb_ws_make(workspace, ws_bytes);
-  const double sqrtw = __builtin_sqrt((double)w);
-  uint64_t positions = (uint64_t)count + (uint64_t)count / 64 + 4 * kZTile;
+  uint64_t positions = zig_positions_for((uint64_t)count);
   for (int attempt = 0; attempt < 4; ++attempt) {
-    const uint64_t tiles = (positions + kZTile - 1) / kZTile;
-    if (tiles > 0xffffff00ULL) return SKB_ERR_UNSUPPORTED;
-    const size_t mark = ws.off;
-    uint64_t* state = (uint64_t*)skb_ws_take(&ws, tiles * 8);
-    uint32_t* ticket = (uint32_t*)skb_ws_take(&ws, 16);
-    int* err = (int*)skb_ws_take(&ws, 16);
-    if (!state || !ticket || !err) return SKB_ERR_WORKSPACE;
-    cudaMemsetAsync(state, 0, tiles * 8, st);
-    cudaMemsetAsync(ticket, 0, 16, st);
-    cudaMemsetAsync(err, 0, 16, st);
-    static int grid = 0;
-    if (!grid) {
-      cudaFuncSetAttribute(gauss_onepass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kZTile * 8);
-      int per = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gauss_onepass_kernel, kZThreads,
-                                                    kZTile * 8);
-      grid = std::max(1, per) * skb_num_sms();
-    }
-    gauss_onepass_kernel<<<(unsigned)std::min<uint64_t>(tiles, (uint64_t)grid), kZThreads,
-                           kZTile * 8, st>>>(key0, key1, 0, (uint64_t)lo, (uint64_t)count, sqrtw,
-                                             W, state, ticket, (uint32_t)tiles, err);
-    uint64_t last = 0;
-    int herr = 0;
-    cudaMemcpyAsync(&last, state + (tiles - 1), 8, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
-    ws.off = mark;
-    if (herr) return SKB_ERR_INTERNAL;  // an attempt longer than 64 words (never observed)
-    if ((last & kZValMask) >= (uint64_t)count) return skb_launch_status(__func__);
-    positions *= 2;
+    skb_ws ws = skb_ws_make(workspace, ws_bytes);
+    uint64_t total = 0;
+    const int rc = zig_generate(key0, key1, 0, positions, (uint64_t)lo, (uint64_t)count, w, W,
+                                &total, &ws, st);
+    if (rc) return rc;
+    if (total >= (uint64_t)count) return 0;
+    positions = (positions * 2 + kZTile - 1) / kZTile * kZTile;  // (never observed)
   }
   return SKB_ERR_INTERNAL;
 }
@@ -517,39 +483,14 @@ extern "C" int skb_gaussian_range(uint64_t key0, uint64_t key1, uint64_t p0, uin
   *count_host = 0;
   if (p1 == p0) return 0;
   skb_ws ws = skb_ws_make(workspace, ws_bytes);
-  const double sqrtw = __builtin_sqrt((double)w);
-  const uint64_t tiles = (p1 - p0) / kZTile;
-  if (tiles > 0xffffff00ULL) return SKB_ERR_UNSUPPORTED;
-  uint64_t* state = (uint64_t*)skb_ws_take(&ws, tiles * 8);
-  uint32_t* ticket = (uint32_t*)skb_ws_take(&ws, 16);
-  int* err = (int*)skb_ws_take(&ws, 16);
-  if (!state || !ticket || !err) return SKB_ERR_WORKSPACE;
-  cudaMemsetAsync(state, 0, tiles * 8, st);
-  cudaMemsetAsync(ticket, 0, 16, st);
-  cudaMemsetAsync(err, 0, 16, st);
-  static int grid = 0;
-  if (!grid) {
-    cudaFuncSetAttribute(gauss_onepass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kZTile * 8);
-    int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gauss_onepass_kernel, kZThreads,
-                                                  kZTile * 8);
-    grid = std::max(1, per) * skb_num_sms();
-  }
-  gauss_onepass_kernel<<<(unsigned)std::min<uint64_t>(tiles, (uint64_t)grid), kZThreads,
-                         kZTile * 8, st>>>(key0, key1, p0, 0, (uint64_t)cap, sqrtw, out, state,
-                                           ticket, (uint32_t)tiles, err);
-  uint64_t last = 0;
-  int herr = 0;
-  cudaMemcpyAsync(&last, state + (tiles - 1), 8, cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
-  if (herr) return SKB_ERR_INTERNAL;
-  *count_host = last & kZValMask;
-  return skb_launch_status(__func__);
+  return zig_generate(key0, key1, p0, p1, 0, (uint64_t)cap, w, out, count_host, &ws, st);
 }
 
+// Workspace for `count` draws (or a range of ~count positions): the slow
+// bitmap, consumed / accepted bitmaps, counts, offsets and the scan scratch.
 extern "C" size_t skb_gaussian_workspace_bytes(int64_t count) {
-  const uint64_t tiles = ((uint64_t)count * 2 + 8 * kZTile) / kZTile + 1;
-  return (size_t)tiles * 8 + 4096;
+  const uint64_t pos = zig_positions_for((uint64_t)std::max<int64_t>(count, 1)) * 2 +
+                       (uint64_t)kZHaloTiles * kZTile;
+  const uint64_t tiles = pos / kZTile + 2;
+  return (size_t)(pos / 32 * 4 + tiles * kZWords * 8 + tiles * 16) + (1u << 20);
 }
