@@ -36,11 +36,22 @@ def _rank_main(rank, world, port, q, kind="sparse"):
         from paper_2209_08722_b200.distributed import Comm
         from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
         from paper_2209_08722_b200.problems import wide_dense_lp
-        lpd = wide_dense_lp(40, 3000, 5)
         comm = Comm()
-        dlp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c), comm=comm)
+        if kind == "sparse_csc":
+            import scipy.sparse as sp
+            from paper_2209_08722_b200.problems import sparse_wide_lp
+            lpd = sparse_wide_lp(100, 20_000, 5, 7)
+            dlp = DeviceLP.from_host(LinearProgram(sp.csr_matrix(lpd.A), lpd.b, lpd.c),
+                                     comm=comm)
+            assert dlp.sparse
+        else:
+            lpd = wide_dense_lp(40, 3000, 5)
+            dlp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c), comm=comm)
         st = IC.make_iterate(dlp, lpd.x0, lpd.y0, lpd.s0)
-        if kind == "gaussian":
+        if kind == "sparse_csc":
+            prm = IC.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5, w=400, s=4,
+                               tol_outer=1e-6, seed=11)
+        elif kind == "gaussian":
             prm = IC.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5,
                                sketch="gaussian", w=160, tol_outer=1e-6, seed=9)
         else:
@@ -48,7 +59,7 @@ def _rank_main(rank, world, port, q, kind="sparse"):
                                tol_outer=1e-7, seed=3)
         rep = IC.solve(dlp, st, prm)
         q.put((rank, rep.outer, [r.inner_iterations for r in rep.steps], rep.mu_trace,
-               rep.objective, rep.x.shape[0], [r.sketch_seed for r in rep.steps]))
+               rep.objective, rep.x.shape[0], [r.sketch_seed for r in rep.steps], lpd.n))
     except Exception as e:  # surface the failure to the parent
         q.put((rank, "error", repr(e)))
         raise
@@ -56,7 +67,8 @@ def _rank_main(rank, world, port, q, kind="sparse"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind", [(2, "sparse"), (3, "sparse"), (2, "gaussian")])
+@pytest.mark.parametrize("world,kind", [(2, "sparse"), (3, "sparse"), (2, "gaussian"),
+                                        (2, "sparse_csc")])
 def test_sharded_solve_matches_reference(world, kind):
     """Sharded sketch + distributed CholeskyQR2 (bucket-row blocks, Gram
     allreduce; world 3 gives uneven blocks) against the reference trajectory."""
@@ -77,13 +89,16 @@ def test_sharded_solve_matches_reference(world, kind):
     if kind == "gaussian":
         with open(os.path.join(GOLDEN, "gaussian_traces.json")) as f:
             gold = json.load(f)["wide"]
+    elif kind == "sparse_csc":
+        with open(os.path.join(GOLDEN, "sparse_traces.json")) as f:
+            gold = json.load(f)["s4"]
     else:
         with open(os.path.join(GOLDEN, "small_traces.json")) as f:
             gold = json.load(f)["feasible"]
-    for rank, outer, inner, mu, obj, nx, seeds in res:
+    for rank, outer, inner, mu, obj, nx, seeds, n_lp in res:
         assert outer == gold["outer"] and inner == gold["inner_iterations"]
         assert seeds == [s["sketch_seed"] for s in gold["steps"]]
-        assert nx == 3000
+        assert nx == n_lp
         dev = np.abs(np.array(mu) - np.array(gold["mu_trace"])) / np.array(gold["mu_trace"])
         # sharded sums change the summation order: same floor as a reordered reference
         assert dev.max() <= 5e-8, dev.max()
