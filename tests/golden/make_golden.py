@@ -303,11 +303,37 @@ def svm_traces():
         json.dump(res, f)
 
 
+def diag_traces():
+    """diag_cond=True (ipm_core.py:576-584): per-step spectrum bounds of the
+    preconditioned normal matrix and cond(AD)^2 on a small LP."""
+    lpd = wide_dense_lp(40, 3000, 5)
+    A = lp_csr(lpd)
+    st = ipm_core.make_iterate(skipm.make_lp(A, lpd.b, lpd.c), lpd.x0, lpd.y0, lpd.s0)
+    prm = ipm_core.IpmParams(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5, w=160, s=4,
+                             tol_outer=1e-6, seed=3, diag_cond=True)
+    rep = ipm_core.solve(skipm.make_lp(A, lpd.b, lpd.c), st, prm)
+    res = {"outer": rep.outer,
+           "steps": [{k: getattr(r, k) for k in ("spectrum_lo", "spectrum_hi", "kappa_sk",
+                                                 "kappa_stan")} for r in rep.steps]}
+    print(f"diag: outer {rep.outer}, kappa_sk max {max(r.kappa_sk for r in rep.steps):.3f}")
+    with open(os.path.join(HERE, "diag_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
+def lp_csr(lpd):
+    import scipy.sparse as sp
+    A = sp.csr_matrix(lpd.A)
+    A.sort_indices()
+    return A
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers", "start", "gaussian",
-                            "sparse", "svm"]
+                            "sparse", "svm", "diag"]
     if "svm" in what:
         svm_traces()
+    if "diag" in what:
+        diag_traces()
     if "sparse" in what:
         sparse_traces()
     if "gaussian" in what:
