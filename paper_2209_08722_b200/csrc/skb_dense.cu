@@ -838,12 +838,52 @@ static int potrf(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStr
   return 0;
 }
 
+static int trtri(const double* L, double* Li, int64_t ld, int Mp, skb_ws* ws, cudaStream_t st);
+
+// Large Mp: two-level blocking. 512-wide outer panels: the diagonal block is
+// factored by potrf (64-wide panels) and inverted by trtri, the panel
+// L21 = A21 L11^-T is ONE 512-deep GEMM into a scratch block, and the trailing
+// update A22 -= L21 L21' ONE lower-tile SYRK — a few large DMMA GEMMs per 512
+// columns instead of 16 small ones (launch- and latency-bound at Mp ~ 1e4).
+constexpr int NBO = 512;
+
+static int potrf_big(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStream_t st) {
+  if (Mp < 4 * NBO) return potrf(G, ld, Mp, status, ws, st);
+  const size_t mark = ws->off;
+  double* Lc = (double*)skb_ws_take(ws, (size_t)NBO * NBO * 8);
+  double* Lci = (double*)skb_ws_take(ws, (size_t)NBO * NBO * 8);
+  double* Pb = (double*)skb_ws_take(ws, (size_t)Mp * NBO * 8);
+  if (!Lc || !Lci || !Pb) return SKB_ERR_WORKSPACE;
+  for (int k0 = 0; k0 < Mp; k0 += NBO) {
+    const int nb = std::min(NBO, Mp - k0);
+    double* D = G + (int64_t)k0 * ld + k0;
+    int rc = potrf(D, ld, nb, status, ws, st);
+    if (rc) return rc;
+    const int rest = Mp - k0 - nb;
+    if (rest <= 0) break;
+    cudaMemcpy2DAsync(Lc, (size_t)nb * 8, D, (size_t)ld * 8, (size_t)nb * 8, nb,
+                      cudaMemcpyDeviceToDevice, st);
+    if ((rc = trtri(Lc, Lci, nb, nb, ws, st))) return rc;
+    double* A21 = G + (int64_t)(k0 + nb) * ld + k0;
+    GemmArgs gp = gemm_args(A21, ld, 0, Lci, nb, 1, Pb, nb, rest, nb, nb, 1.0, 0.0, 0);
+    gp.tri_b = 2;  // opB = L11^-T (upper)
+    if ((rc = gemm_launch(gp, 1, ws, st))) return rc;
+    cudaMemcpy2DAsync(A21, (size_t)ld * 8, Pb, (size_t)nb * 8, (size_t)nb * 8, rest,
+                      cudaMemcpyDeviceToDevice, st);
+    double* T = G + (int64_t)(k0 + nb) * ld + k0 + nb;
+    GemmArgs g = gemm_args(Pb, nb, 0, Pb, nb, 1, T, ld, rest, rest, nb, -1.0, 1.0, 1);
+    if ((rc = gemm_launch(g, 1, ws, st))) return rc;
+  }
+  ws->off = mark;
+  return 0;
+}
+
 extern "C" int skb_potrf(double* G, int64_t ld, int32_t Mp, int* status, void* workspace,
                          size_t ws_bytes, void* stream) {
   if (Mp % NB) return SKB_ERR_ARG;
   skb_ws ws = skb_ws_make(workspace, ws_bytes);
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = potrf(G, ld, Mp, status, &ws, st);
+  int rc = potrf_big(G, ld, Mp, status, &ws, st);
   if (rc) return rc;
   zero_upper_kernel<<<(unsigned)(((int64_t)Mp * Mp + 255) / 256), 256, 0, st>>>(G, ld, Mp);
   return skb_launch_status(__func__);
@@ -953,7 +993,7 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
   cudaMemsetAsync(status, 0, 64, st);
   if ((rc = gram(X))) return rc;
   diag_stats_kernel<<<1, 1024, 0, st>>>(G, ld, m, dstat, 0);
-  if ((rc = potrf(G, ld, Mp, status, &ws, st))) return rc;
+  if ((rc = potrf_big(G, ld, Mp, status, &ws, st))) return rc;
   cudaMemcpyAsync(&hst, status, 4, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(hstat, dstat, 8, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
@@ -965,7 +1005,7 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
     cudaMemsetAsync(status, 0, 64, st);
     if ((rc = gram(X))) return rc;
     add_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(G, ld, m, shift);
-    if ((rc = potrf(G, ld, Mp, status, &ws, st))) return rc;
+    if ((rc = potrf_big(G, ld, Mp, status, &ws, st))) return rc;
   }
   // potrf leaves the strict upper part zero (G was cleared before the lower-tile
   // Gram, diagonal blocks are rewritten, trailing updates stay on lower tiles).
@@ -981,7 +1021,7 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
     if ((rc = gemm_launch(gy, 1, &ws, st))) return rc;
     Z = Y;
     if ((rc = gram(Y))) return rc;
-    if ((rc = potrf(G, ld, Mp, status, &ws, st))) return rc;
+    if ((rc = potrf_big(G, ld, Mp, status, &ws, st))) return rc;
     if ((rc = trtri(G, L2i, ld, Mp, &ws, st))) return rc;
     diag_accum_kernel<<<(m + 255) / 256, 256, 0, st>>>(G, ld, m, dprod, 0);  // diag(L1 L2)
     // Linv = L2i * L1i (lower x lower; tiles above the diagonal are skipped -> clear first)

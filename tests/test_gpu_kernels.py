@@ -229,3 +229,26 @@ def test_weighted_gram(K):
     ref = (A * wts) @ A.T
     out = np.tril(_h(G))
     assert np.max(np.abs(out - np.tril(ref))) <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("Mp", [192, 1024, 2560])
+def test_potrf_trtri_against_numpy(K, Mp):
+    """skb_potrf (64-wide panels; two-level 512-wide blocking from Mp = 2048)
+    and skb_trtri against numpy's Cholesky / inverse on an SPD Gram matrix."""
+    from paper_2209_08722_b200 import _lib
+    from paper_2209_08722_b200.runtime import stream_ptr, workspace
+    g = np.random.Generator(np.random.Philox(Mp))
+    X = g.standard_normal((Mp + 200, Mp))
+    S = X.T @ X
+    G = _t(np.tril(S))
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(Mp, Mp + 200)))
+    _lib.call("skb_potrf", G, Mp, Mp, st, ws, cap, stream_ptr())
+    L = np.tril(_h(G))
+    assert int(st.item()) == 0
+    Lref = np.linalg.cholesky(S)
+    assert np.max(np.abs(L - Lref)) <= 1e-10 * np.abs(Lref).max()
+    Li = torch.zeros_like(G)
+    _lib.call("skb_trtri", G, Li, Mp, Mp, ws, cap, stream_ptr())
+    E = np.tril(_h(Li)) @ Lref - np.eye(Mp)
+    assert np.max(np.abs(E)) <= 1e-9

@@ -35,3 +35,12 @@ print("largest host gaps before a call (us), call duration (us), call:")
 for g, d, n in big:
     print(f"{g * 1e6:9.1f} {d * 1e6:9.1f}  {n}")
 print("sum of gaps (ms):", sum(r[0] for r in rows) * 1e3, "calls", len(rows))
+# the ordered sequence of one step (largest gaps flagged)
+print("--- sequence (gap_us, dur_us, call) for the first ~70 calls of the 2nd step ---")
+marks = [i for i, (_, _, nm) in enumerate(log) if nm == "skb_step_prep"]
+if len(marks) >= 2:
+    i0, i1 = marks[1], marks[2] if len(marks) > 2 else len(log)
+    prev = log[i0 - 1][1]
+    for t0, t1, nm in log[i0 - 3:i1]:
+        print(f"{(t0 - prev) * 1e6:9.1f} {(t1 - t0) * 1e6:9.1f}  {nm}")
+        prev = t1
