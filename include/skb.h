@@ -221,6 +221,17 @@ int skb_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, double alp
              int64_t ldc, int32_t lower_only, int32_t batch, int64_t strideA, int64_t strideB,
              int64_t strideC, void* workspace, size_t ws_bytes, void* stream);
 
+/* The same product emulated in FP64 on the INT8 tensor cores (CRT over 16
+ * moduli, csrc/skb_ozaki.cu); lower_only writes j <= i only. skb_gemm routes
+ * large unbatched products here (SKB_GEMM_EMU=0 disables). Returns
+ * SKB_ERR_UNSUPPORTED when cuBLASLt cannot be loaded or the workspace is short. */
+int skb_gemm_ozaki(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, double alpha,
+                   const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                   double* C, int64_t ldc, int32_t lower_only, void* workspace, size_t ws_bytes,
+                   void* stream);
+size_t skb_gemm_ozaki_workspace_bytes(int32_t M, int32_t N, int32_t K);
+int64_t skb_gemm_ozaki_calls(void);
+
 /* Blocked Cholesky (lower, in place) and triangular inverse; Mp % 64 == 0.
  * status: device int, SKB_ST_CHOL_FAIL on a nonpositive pivot. */
 int skb_potrf(double* G, int64_t ld, int32_t Mp, int* status, void* workspace, size_t ws_bytes,

@@ -47,7 +47,7 @@ def parse_header(path: str = HEADER) -> dict:
     text = re.sub(r"/\*.*?\*/", " ", text, flags=re.S)
     text = re.sub(r"//[^\n]*", " ", text)
     protos = {}
-    for m in re.finditer(r"\b(int32_t|int|size_t|void)\s+(skb_\w+)\s*\(([^)]*)\)\s*;", text):
+    for m in re.finditer(r"\b(int32_t|int64_t|int|size_t|void)\s+(skb_\w+)\s*\(([^)]*)\)\s*;", text):
         ret, name, args = m.group(1), m.group(2), m.group(3)
         argtypes = []
         for a in [a.strip() for a in args.split(",") if a.strip() and a.strip() != "void"]:

@@ -25,6 +25,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-I", os.path.join(ROOT, "include"), "-I", OBJ]
 # generated at build time from numpy's own tables (see ziggurat_tables.py)
 ZIG_HEADER = os.path.join(OBJ, "skb_ziggurat_tables.h")
+OZ_HEADER = os.path.join(OBJ, "skb_ozaki_tables.h")  # CRT tables (ozaki_tables.py)
 # Elementwise step kernels follow numpy's rounding exactly: no FMA contraction.
 PER_FILE = {"skb_step.cu": ["-fmad=false"]}
 
@@ -46,7 +47,7 @@ def _stale(obj: str, src: str) -> bool:
     t = os.path.getmtime(obj)
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC)
                     if f.endswith((".cuh", ".h"))] + [os.path.join(ROOT, "include", "skb.h"),
-                                                      ZIG_HEADER]
+                                                      ZIG_HEADER, OZ_HEADER]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -68,6 +69,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     sys.path.insert(0, HERE)
     from ziggurat_tables import write_header
     write_header(ZIG_HEADER)
+    import ozaki_tables
+    ozaki_tables.write_header(OZ_HEADER)
     if force:
         for f in os.listdir(OBJ):
             os.remove(os.path.join(OBJ, f))
@@ -76,7 +79,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if force or not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT)
                                                for o in objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", OUT] + objs
+        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", OUT] + objs + ["-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -16,6 +16,7 @@
 // FP64. Everything else here is latency- or HBM-bound.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "skb_common.cuh"
 #include "skb_internal.h"
@@ -672,9 +673,48 @@ using namespace skb;
 
 // ----------------------------------------------------------------- host API
 
+// Large unbatched products go to the INT8-tensor-core FP64 emulation
+// (skb_ozaki.cu) when its cost model beats DMMA: 16 INT8 GEMMs at ~2.4 POP/s
+// plus the HBM passes of the residue split and the CRT, against DMMA at
+// ~30 TFLOP/s on the (triangle-trimmed) flops. SKB_GEMM_EMU=0 disables it,
+// SKB_GEMM_EMU=2 forces it for every eligible shape (tests).
+static int try_emulated(const GemmArgs& g, int nbatch, skb_ws* ws, cudaStream_t st) {
+  const char* env = getenv("SKB_GEMM_EMU");
+  const int mode = env ? atoi(env) : 1;
+  if (!mode || nbatch != 1 || g.K < 256) return 1;
+  const double M = g.M, N = g.N, K = g.K;
+  double dm = 2.0 * M * N * K;
+  if (g.lower_only) dm *= 0.5;
+  if (g.tri_a || g.tri_b) dm *= 0.5;
+  const double t_dmma = dm / 30e12;
+  // triangles are exploited by 1280-wide slabs (~1/(2s) waste) in the emulation
+  const double t_emu = 16.0 * 1.1 * dm / 2.4e15 + ((M + N) * K * 26.0 + M * N * 80.0) / 5e12 +
+                       60e-6;
+  if (mode == 1 && !(t_emu < 0.8 * t_dmma)) return 1;
+  skb_oz_args o{};
+  o.a = g.ta ? skb_oz_operand{g.A, 1, g.lda} : skb_oz_operand{g.A, g.lda, 1};
+  o.b = g.tb ? skb_oz_operand{g.B, g.ldb, 1} : skb_oz_operand{g.B, 1, g.ldb};
+  o.kscale = g.kscale;
+  o.C = g.C;
+  o.ldc = g.ldc;
+  o.M = g.M;
+  o.N = g.N;
+  o.K = g.K;
+  o.alpha = g.alpha;
+  o.beta = g.beta;
+  o.lower_only = g.lower_only;
+  o.tri_a = g.tri_a;
+  o.tri_b = g.tri_b;
+  return skb_oz_gemm(o, ws, st);
+}
+
 static int gemm_launch(const GemmArgs& base, int nbatch, skb_ws* ws, cudaStream_t st) {
   GemmArgs g = base;
   if (g.M <= 0 || g.N <= 0) return 0;
+  {
+    const int rc = try_emulated(g, nbatch, ws, st);
+    if (rc <= 0) return rc;
+  }
   const bool pipe = pipe_ok(g);
   const int bmt = pipe ? PBM : GBM, bnt = pipe ? PBN : GBN;
   const int tm = (g.M + bmt - 1) / bmt, tn = (g.N + bnt - 1) / bnt;
@@ -950,9 +990,12 @@ extern "C" int skb_trtri(const double* L, double* Li, int64_t ld, int32_t Mp, vo
 extern "C" size_t skb_factor_workspace_bytes(int32_t m, int32_t w) {
   const size_t Mp = (size_t)round_pad(m);
   const size_t ldx = (size_t)(m + (m & 1));
-  // G, L1inv, L2inv, Y + GEMM split partials (<= 64 * 2 * 148 tiles) + trtri temp
-  const size_t split = 4 * Mp * Mp * 8;  // split-K partials
-  return 3 * Mp * Mp * 8 + (size_t)w * ldx * 8 + Mp * Mp * 4 + split + 16 * 256;
+  // G, L1inv, L2inv, Y + trtri temp, then room for one GEMM's scratch: DMMA
+  // split-K partials or the INT8 emulation's residues + INT32 slab (Gram: one
+  // shared residue set over K = w; Y = X L1^-T: both over K = m).
+  const size_t split = 4 * Mp * Mp * 8;
+  const size_t emu = std::max(skb_oz_bytes(m, m, w, true), skb_oz_bytes(w, m, m, false));
+  return 3 * Mp * Mp * 8 + (size_t)w * ldx * 8 + Mp * Mp * 4 + std::max(split, emu) + 16 * 256;
 }
 
 // CholeskyQR2 of X' (X: w x m bucket-major, ldx). Outputs (Mp x Mp, ld = Mp):

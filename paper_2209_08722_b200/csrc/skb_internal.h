@@ -51,3 +51,24 @@ static inline int skb_launch_status(const char* where) {
           cudaGetErrorString(e));
   return SKB_ERR_CUDA;
 }
+
+// FP64 GEMM on the INT8 tensor cores (skb_ozaki.cu). Operand x has R rows over
+// K with element (r, k) at p[r * sr + k * sk]; C[i][j] (row-major, ldc) =
+// alpha sum_k a(i,k) kscale[k] b(j,k) + beta C. Returns 0 done, 1 not
+// applicable (workspace / cuBLASLt unavailable: the caller runs DMMA), < 0 error.
+struct skb_oz_operand {
+  const double* p;
+  int64_t sr, sk;
+};
+struct skb_oz_args {
+  skb_oz_operand a, b;
+  const double* kscale;
+  double* C;
+  int64_t ldc;
+  int M, N, K;
+  double alpha, beta;
+  int lower_only;
+  int tri_a, tri_b;  // as GemmArgs: opA lower (1) / upper (2), opB lower (1) / upper (2)
+};
+int skb_oz_gemm(const skb_oz_args& g, skb_ws* ws, cudaStream_t st);
+size_t skb_oz_bytes(int M, int N, int K, bool share);

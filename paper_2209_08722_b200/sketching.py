@@ -234,8 +234,11 @@ def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = 
                       ldx, ws, cap, stream_ptr())
     else:  # dense Gaussian: one DMMA GEMM, X = W' D A' (sketching.py:158-159)
         Ad = lp.dense_A()
-        # + room for up to 8 split-K partials of the w x m product
-        ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(m, W.w)) + 8 * 8 * m * W.w)
+        # + room for up to 8 split-K partials of the w x m product, or for the
+        # INT8 emulation's residues in K chunks of 65536 (csrc/skb_ozaki.cu)
+        L = _lib.lib()
+        need = max(8 * 8 * m * W.w, int(L.skb_gemm_ozaki_workspace_bytes(W.w, m, min(Ad.n, 65536))))
+        ws, cap = workspace(int(L.skb_factor_workspace_bytes(m, W.w)) + need)
         _lib.call("skb_gaussian_apply", Ad.cols, m, Ad.n, Ad.lda, d, W.dense, W.w, X, ldx, ws,
                   cap, stream_ptr())
     if ldx != m:

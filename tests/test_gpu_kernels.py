@@ -191,13 +191,15 @@ GEMM_CASES = [(129, 65, 37, 0), (300, 200, 1000, 0), (1000, 1000, 4000, 1), (64,
 
 @pytest.mark.parametrize("M,N,Kd,lower", GEMM_CASES)
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("pipe", [True, False])
+@pytest.mark.parametrize("pipe", ["pipe", "nopipe", "emu"])
 def test_gemm_against_numpy(K, monkeypatch, M, N, Kd, lower, ta, tb, pipe):
-    """skb_gemm (both the cp.async 128x64 kernel and the register-staged
-    fallback) against numpy fp64; error bound 1e-13 * sum|a||b|."""
+    """skb_gemm (the cp.async 128x64 DMMA kernel, the register-staged fallback,
+    and the INT8 emulation forced for K >= 256) against numpy fp64; error bound
+    1e-13 * sum|a||b|."""
     from paper_2209_08722_b200 import _lib
     from paper_2209_08722_b200.runtime import stream_ptr, workspace
-    if not pipe:
+    monkeypatch.setenv("SKB_GEMM_EMU", "2" if pipe == "emu" else "0")
+    if pipe == "nopipe":
         monkeypatch.setenv("SKB_GEMM_NOPIPE", "1")
     g = np.random.Generator(np.random.Philox(M * 7 + N + Kd))
     opa = g.standard_normal((M, Kd))
@@ -206,7 +208,7 @@ def test_gemm_against_numpy(K, monkeypatch, M, N, Kd, lower, ta, tb, pipe):
     B = opb.T.copy() if tb else opb.copy()
     C0 = g.standard_normal((M, N))
     Cd = _t(C0)
-    ws, cap = workspace(1 << 26)
+    ws, cap = workspace((1 << 26) + int(_lib.lib().skb_gemm_ozaki_workspace_bytes(M, N, Kd)))
     _lib.call("skb_gemm", ta, tb, M, N, Kd, 0.5, _t(A), A.shape[1], _t(B), B.shape[1], -1.0, Cd, N,
               lower, 1, 0, 0, 0, ws, cap, stream_ptr())
     ref = 0.5 * opa @ opb - C0
@@ -231,12 +233,16 @@ def test_weighted_gram(K):
     assert np.max(np.abs(out - np.tril(ref))) <= 1e-12 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("Mp", [192, 1024, 2560])
-def test_potrf_trtri_against_numpy(K, Mp):
+@pytest.mark.parametrize("Mp,emu", [(192, "0"), (1024, "0"), (2560, "0"), (1024, "2"),
+                                    (2560, "2")])
+def test_potrf_trtri_against_numpy(K, monkeypatch, Mp, emu):
     """skb_potrf (64-wide panels; two-level 512-wide blocking from Mp = 2048)
-    and skb_trtri against numpy's Cholesky / inverse on an SPD Gram matrix."""
+    and skb_trtri against numpy's Cholesky / inverse on an SPD Gram matrix;
+    emu "2" routes every GEMM with K >= 256 (triangular operands included)
+    through the INT8 emulation."""
     from paper_2209_08722_b200 import _lib
     from paper_2209_08722_b200.runtime import stream_ptr, workspace
+    monkeypatch.setenv("SKB_GEMM_EMU", emu)
     g = np.random.Generator(np.random.Philox(Mp))
     X = g.standard_normal((Mp + 200, Mp))
     S = X.T @ X

@@ -108,8 +108,11 @@ def _factor_case(P, m, n, w, s, span=2.0, seed=0):
 @pytest.mark.parametrize("m,n,w,s,span", [(20, 2000, 80, 4, 2.0), (100, 10_000, 400, 1, 3.0),
                                           (300, 6000, 1200, 4, 4.0), (1000, 12_000, 4000, 1, 2.0),
                                           (65, 3000, 260, 2, 6.0)])
-def test_factor_inverse_and_pinv(P, m, n, w, s, span):
+@pytest.mark.parametrize("emu", ["1", "2"])
+def test_factor_inverse_and_pinv(P, monkeypatch, m, n, w, s, span, emu):
+    """emu "2": every factor GEMM with K >= 256 on the INT8 emulation."""
     from paper_2209_08722_b200 import preconditioning as PC
+    monkeypatch.setenv("SKB_GEMM_EMU", emu)
     g, A, d, lp, W, f, Wo, fo = _factor_case(P, m, n, w, s, span)
     r = g.standard_normal(m)
     z = _h(PC.apply_inv(f, _t(r)))
@@ -253,7 +256,9 @@ def test_small_lp_trajectories_both_modes(P, monkeypatch):
     _check_trace(rep, gold["infeasible"], _reordered_oracle(monkeypatch, lpd, start=start, **kw))
 
 
-def test_config1_trajectory_s4(P, monkeypatch):
+@pytest.mark.parametrize("emu", ["1", "2"])
+def test_config1_trajectory_s4(P, monkeypatch, emu):
+    monkeypatch.setenv("SKB_GEMM_EMU", emu)
     with open(os.path.join(GOLDEN, "c1_traces.json")) as f:
         gold = json.load(f)
     lpd = wide_dense_lp(100, 10_000, 0)
@@ -402,10 +407,13 @@ def test_gaussian_sketch_bit_exact(P):
         np.max(np.abs(_h(part.dense) - full[1234:4321])) <= 1e-15
 
 
-@pytest.mark.parametrize("name", ["wide", "illcond"])
-def test_gaussian_sketch_trajectories(P, monkeypatch, name):
-    """sketch='gaussian' solves (DMMA GEMM ADW) vs the reference, incl. the c5
-    ill-conditioned generator A = diag(r) G (kappa(ADW) up to ~1e9)."""
+@pytest.mark.parametrize("name,emu", [("wide", "1"), ("illcond", "1"), ("wide", "2"),
+                                      ("illcond", "2")])
+def test_gaussian_sketch_trajectories(P, monkeypatch, name, emu):
+    """sketch='gaussian' solves (GEMM ADW) vs the reference, incl. the c5
+    ill-conditioned generator A = diag(r) G (kappa(ADW) up to ~1e9); emu "2"
+    runs the sketch GEMM and the factor on the INT8 emulation."""
+    monkeypatch.setenv("SKB_GEMM_EMU", emu)
     from paper_2209_08722_b200.problems import ill_conditioned_lp
     with open(os.path.join(GOLDEN, "gaussian_traces.json")) as f:
         gold = json.load(f)[name]
