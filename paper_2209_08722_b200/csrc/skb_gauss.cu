@@ -438,8 +438,11 @@ static int zig_generate(uint64_t k0, uint64_t k1, uint64_t P0, uint64_t P1, uint
   return skb_launch_status("zig_generate");
 }
 
+// numpy's ziggurat consumes 1.0220 words per draw on average (fast-path
+// acceptance 98.9%; slow attempts take extra words and may restart), with a
+// relative spread ~1e-5 at 1e9 draws: 1 + 1/32 covers it with one pass.
 static uint64_t zig_positions_for(uint64_t count) {
-  const uint64_t p = count + count / 64 + 4 * (uint64_t)kZTile;
+  const uint64_t p = count + count / 32 + 8 * (uint64_t)kZTile;
   return (p + kZTile - 1) / kZTile * kZTile;
 }
 
@@ -464,7 +467,7 @@ extern "C" int skb_gaussian_sketch(uint64_t key0, uint64_t key1, int64_t lo, int
                                 &total, &ws, st);
     if (rc) return rc;
     if (total >= (uint64_t)count) return 0;
-    positions = (positions * 2 + kZTile - 1) / kZTile * kZTile;  // (never observed)
+    positions = (positions + positions / 16 + kZTile - 1) / kZTile * kZTile;  // (never observed)
   }
   return SKB_ERR_INTERNAL;
 }
