@@ -880,15 +880,17 @@ static int potrf(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStr
 
 static int trtri(const double* L, double* Li, int64_t ld, int Mp, skb_ws* ws, cudaStream_t st);
 
-// Large Mp: two-level blocking. 512-wide outer panels: the diagonal block is
-// factored by potrf (64-wide panels) and inverted by trtri, the panel
-// L21 = A21 L11^-T is ONE 512-deep GEMM into a scratch block, and the trailing
-// update A22 -= L21 L21' ONE lower-tile SYRK — a few large DMMA GEMMs per 512
-// columns instead of 16 small ones (launch- and latency-bound at Mp ~ 1e4).
-constexpr int NBO = 512;
+// Large Mp: two-level blocking. NBO-wide outer panels (512 / 1024 / 2048 as
+// Mp grows): the diagonal block is factored by potrf (64-wide panels) and
+// inverted by trtri, the panel L21 = A21 L11^-T is ONE NBO-deep GEMM into a
+// scratch block, and the trailing update A22 -= L21 L21' ONE lower-tile SYRK.
+// A few large GEMMs per NBO columns instead of NBO/64 small ones; from
+// NBO = 1024 they are long enough for the INT8 emulation's cost model.
+static int outer_block(int Mp) { return Mp >= 8192 ? 2048 : (Mp >= 4096 ? 1024 : 512); }
 
 static int potrf_big(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStream_t st) {
-  if (Mp < 4 * NBO) return potrf(G, ld, Mp, status, ws, st);
+  if (Mp < 2048) return potrf(G, ld, Mp, status, ws, st);
+  const int NBO = outer_block(Mp);
   const size_t mark = ws->off;
   double* Lc = (double*)skb_ws_take(ws, (size_t)NBO * NBO * 8);
   double* Lci = (double*)skb_ws_take(ws, (size_t)NBO * NBO * 8);

@@ -234,7 +234,7 @@ def test_weighted_gram(K):
 
 
 @pytest.mark.parametrize("Mp,emu", [(192, "0"), (1024, "0"), (2560, "0"), (1024, "2"),
-                                    (2560, "2")])
+                                    (2560, "2"), (4160, "1"), (8192, "1")])
 def test_potrf_trtri_against_numpy(K, monkeypatch, Mp, emu):
     """skb_potrf (64-wide panels; two-level 512-wide blocking from Mp = 2048)
     and skb_trtri against numpy's Cholesky / inverse on an SPD Gram matrix;
