@@ -222,15 +222,18 @@ __global__ void __launch_bounds__(256) split_kernel(const double* __restrict__ p
 #pragma unroll
     for (int l = 0; l < NM; ++l) {
       const double pl = tab.p[l], pi = tab.pinv[l], c26 = tab.c26[l];
-      uint32_t pack = 0;
+      uint32_t ri[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double v = fma(ah[u], c26, al[u]);
         const double q = fma(v, pi, kMagic) - kMagic;
-        const uint32_t ri = (uint32_t)__double2loint(fma(-q, pl, v) + kMagic);
-        pack |= (ri & 0xffu) << (8 * u);
+        ri[u] = (uint32_t)__double2loint(fma(-q, pl, v) + kMagic);  // low byte = residue
       }
-      *reinterpret_cast<uint32_t*>(o + l * lstride) = pack;
+      // 4 low bytes -> one word: 3 byte permutes
+      const uint32_t pack = __byte_perm(__byte_perm(ri[0], ri[1], 0x0040),
+                                        __byte_perm(ri[2], ri[3], 0x0040), 0x5410);
+      *reinterpret_cast<uint32_t*>(o) = pack;
+      o += lstride;
     }
   }
 }
@@ -256,7 +259,10 @@ __global__ void __launch_bounds__(256) crt_kernel(const int32_t* __restrict__ c3
   const int32_t* src = c32 + (int64_t)ii * ldc32 + jj;
   int c[NM];
 #pragma unroll
-  for (int l = 0; l < NM; ++l) c[l] = __ldg(src + l * mstride);  // all loads in flight
+  for (int l = 0; l < NM; ++l) {  // all loads in flight
+    c[l] = __ldg(src);
+    src += mstride;
+  }
   constexpr double kI2D = 4503601774854144.0;  // 2^52 + 2^31
   double q = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
 #pragma unroll
