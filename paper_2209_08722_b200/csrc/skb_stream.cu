@@ -844,7 +844,11 @@ extern "C" size_t skb_stream_workspace_bytes(int64_t m) {
 // follows the hardware's atomic arbitration (tolerance parity, not bitwise).
 namespace skb {
 
-constexpr int kCscThreads = 512;
+// 1024 threads (32 warps) hide the dependent colptr -> rowidx -> z loads of the
+// one-CTA-per-SM normal apply (0.62 -> 0.48 ms at c4); the axpy-only passes run
+// two 512-thread CTAs per SM (their single m-vector leaves room for two).
+// (Gathering z through L1 to fit two 1024-thread CTAs doubled the time.)
+constexpr int kCscThreads = 1024;
 
 template <class Op>
 __global__ void __launch_bounds__(kCscThreads)
@@ -889,7 +893,8 @@ static int run_csc(const int64_t* colptr, const int32_t* rowidx, const double* v
   if (smem > 220 * 1024) return SKB_ERR_UNSUPPORTED;  // m <= 14080 with both vectors
   const int per_sm = smem <= 100 * 1024 ? 2 : 1;
   int grid = skb_num_sms() * per_sm;
-  const int64_t need = (n + kCscThreads - 1) / kCscThreads;
+  const int thr = (Op::kDot || !Op::kAxpy) ? kCscThreads : 512;
+  const int64_t need = (n + thr - 1) / thr;
   if (need < grid) grid = (int)std::max<int64_t>(1, need);
   double* part = nullptr;
   if (Op::kAxpy) {
@@ -905,7 +910,7 @@ static int run_csc(const int64_t* colptr, const int32_t* rowidx, const double* v
     configured = smem;
   }
   if (n > 0)
-    kern<<<grid, kCscThreads, smem, st>>>(colptr, rowidx, vals, m, n, z, part, op, gate);
+    kern<<<grid, thr, smem, st>>>(colptr, rowidx, vals, m, n, z, part, op, gate);
   if (Op::kAxpy)
     reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, n > 0 ? grid : 0, m, sub, out,
                                                           gate);
