@@ -15,7 +15,7 @@ from . import _lib
 from .errors import DimensionMismatch, NonpositivePoint, StaleFactor
 from .lp_model import reduce_call
 from .preconditioning import PreconditionerFactor, apply_pinv_adw, reconstruct
-from .runtime import F64, stream_ptr
+from .runtime import F64, stream_ptr, to_host
 from .sketching import SketchOperator
 
 
@@ -68,7 +68,7 @@ def compute_v(f: PreconditionerFactor, W: SketchOperator, x: torch.Tensor, s: to
     inf_norm = None
     if scale is None:
         inf_norm = reduce_call("skb_vec_stats", 4, infeas, None, f.m)
-    host = torch.cat([st, vst] + ([inf_norm] if inf_norm is not None else [])).cpu().numpy()
+    host = to_host(torch.cat([st, vst] + ([inf_norm] if inf_norm is not None else [])))
     denom = scale if scale is not None else math.sqrt(host[8]) + 1.0
     if denom <= 0.0:
         denom = 1.0

@@ -1039,9 +1039,12 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
   if ((rc = gram(X))) return rc;
   diag_stats_kernel<<<1, 1024, 0, st>>>(G, ld, m, dstat, 0);
   if ((rc = potrf_big(G, ld, Mp, status, &ws, st))) return rc;
-  cudaMemcpyAsync(&hst, status, 4, cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(hstat, dstat, 8, cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  {
+    skb_readback rb(st);
+    rb.add(&hst, status, 4);
+    rb.add(hstat, dstat, 8);
+    if (rb.sync() != cudaSuccess) return SKB_ERR_CUDA;
+  }
   if (hst & ST_CHOL_FAIL) {
     // shifted CholeskyQR: s = 11 (m w + m (m + 1)) u ||X||_F^2
     shifted = true;
@@ -1087,9 +1090,12 @@ extern "C" int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32
     if ((rc = trtri(Linv, Lfac, ld, Mp, &ws, st))) return rc;
   }
   vec_minmax_kernel<<<1, 1024, 0, st>>>(dprod, m, dstat);
-  cudaMemcpyAsync(hstat, dstat, 24, cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&hst, status, 4, cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  {
+    skb_readback rb(st);
+    rb.add(hstat, dstat, 24);
+    rb.add(&hst, status, 4);
+    if (rb.sync() != cudaSuccess) return SKB_ERR_CUDA;
+  }
   if (stats_host) {
     stats_host[0] = hstat[1];
     stats_host[1] = hstat[2];

@@ -431,9 +431,10 @@ static int zig_generate(uint64_t k0, uint64_t k1, uint64_t P0, uint64_t P1, uint
     zig_emit_kernel<<<(unsigned)std::min<int64_t>(tiles, 8LL * sms), kZThreads, 0, st>>>(
         k0, k1, P0, tiles, gskip, gacc, offs, lo, need, __builtin_sqrt((double)w), out);
   int herr = 0;
-  cudaMemcpyAsync(total, offs + tiles, 8, cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  skb_readback rb(st);
+  rb.add(total, offs + tiles, 8);
+  rb.add(&herr, err, 4);
+  if (rb.sync() != cudaSuccess) return SKB_ERR_CUDA;
   if (herr) return SKB_ERR_INTERNAL;  // an attempt longer than 64 words (never observed)
   return skb_launch_status("zig_generate");
 }

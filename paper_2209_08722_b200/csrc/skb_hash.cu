@@ -229,8 +229,9 @@ static int lemire_draw(uint64_t k0, uint64_t k1, uint64_t* pos, uint32_t bound, 
     lemire_emit_kernel<<<(unsigned)tiles, kHashThreads, 0, st>>>(k0, k1, q0, q1, bound, thr,
                                                                  tile_off, cnt, out, scal + 1);
     uint64_t h[2];
-    cudaMemcpyAsync(h, scal, 16, cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
+    skb_readback rb(st);
+    rb.add(h, scal, 16);
+    cudaError_t e = rb.sync();
     ws->off = mark;
     if (e != cudaSuccess) return SKB_ERR_CUDA;
     if (h[0] >= cnt) {
@@ -254,8 +255,9 @@ static int compact_flags(const uint32_t* flag, int64_t n, const int64_t* rows, i
   scan_u32_kernel<<<1, 1024, 0, st>>>(tc, to, (int)tiles, tot);
   flag_emit_kernel<<<(unsigned)tiles, 1024, 0, st>>>(flag, n, to, rows, out);
   uint64_t h = 0;
-  cudaMemcpyAsync(&h, tot, 8, cudaMemcpyDeviceToHost, st);
-  cudaError_t e = cudaStreamSynchronize(st);
+  skb_readback rb(st);
+  rb.add(&h, tot, 8);
+  cudaError_t e = rb.sync();
   ws->off = mark;
   if (e != cudaSuccess) return SKB_ERR_CUDA;
   *count = (int64_t)h;

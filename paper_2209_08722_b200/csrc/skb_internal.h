@@ -72,3 +72,44 @@ struct skb_oz_args {
 };
 int skb_oz_gemm(const skb_oz_args& g, skb_ws* ws, cudaStream_t st);
 size_t skb_oz_bytes(int M, int N, int K, bool share);
+
+#include <string.h>
+
+// Small device -> host readbacks (status words, counts, a few statistics)
+// through the calling thread's pinned buffer: a pageable destination makes the
+// driver stage the copy, which costs tens of microseconds more per readback
+// on a path that does several per IPM step. Usage: add() the copies, then
+// sync() once; the values land in the caller's (pageable) variables.
+struct skb_readback {
+  struct Item {
+    void* dst;
+    size_t at, n;
+  };
+  Item items[8];
+  int k = 0;
+  size_t off = 0;
+  char* pin = nullptr;
+  cudaStream_t st;
+  explicit skb_readback(cudaStream_t s) : st(s) {
+    thread_local char* buf = nullptr;
+    if (!buf && cudaHostAlloc((void**)&buf, 4096, cudaHostAllocDefault) != cudaSuccess) {
+      buf = nullptr;
+      cudaGetLastError();
+    }
+    pin = buf;
+  }
+  void add(void* dst, const void* src, size_t n) {
+    if (!pin || k == 8 || off + n > 4096) {  // no pinned room: direct (staged) copy
+      cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st);
+      return;
+    }
+    cudaMemcpyAsync(pin + off, src, n, cudaMemcpyDeviceToHost, st);
+    items[k++] = Item{dst, off, n};
+    off += (n + 15) & ~(size_t)15;
+  }
+  cudaError_t sync() {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    for (int i = 0; i < k; ++i) memcpy(items[i].dst, pin + items[i].at, items[i].n);
+    return e;
+  }
+};

@@ -276,8 +276,9 @@ extern "C" int skb_pcg_solve(const double* A, int64_t m, int64_t n, int64_t lda,
     if ((rc = skb_pcg_step_b(r, z, q, m, t_max, state, trace, stream))) return rc;
   }
   PcgState h;
-  cudaMemcpyAsync(&h, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return SKB_ERR_CUDA;
+  skb_readback rb(st);
+  rb.add(&h, S, sizeof(PcgState));
+  if (rb.sync() != cudaSuccess) return SKB_ERR_CUDA;
   if (trace_host && h.iters + 1 > 0) {
     cudaMemcpy(trace_host, trace, sizeof(double) * (size_t)(h.iters + 1), cudaMemcpyDeviceToHost);
   }

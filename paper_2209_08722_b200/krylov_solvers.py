@@ -20,7 +20,7 @@ from . import _lib
 from .errors import Breakdown, NonpositiveScaling
 from .lp_model import DeviceLP, reduce_call
 from .preconditioning import PreconditionerFactor, apply_inv
-from .runtime import F64, stream_ptr, workspace
+from .runtime import F64, stream_ptr, to_host, workspace
 
 
 class NormalOperator:
@@ -144,7 +144,7 @@ def _pcg_generic(op, f, p, dy, t_max, tol, B):
     state_view = B.state.view(torch.int32)
     for _ in range(t_max):
         if not gated:
-            if int(state_view[8].item()):  # stop flag (host check per step)
+            if int(to_host(state_view[8:9])[0]):  # stop flag (host check per step)
                 break
             Aq.copy_(op.apply(q))
         else:
@@ -153,17 +153,17 @@ def _pcg_generic(op, f, p, dy, t_max, tol, B):
         _lib.call("skb_rowdot_gemv", f.Linv, f.ld, m, m, 1, r, t, _Ptr(stop_ptr), sp_)
         _lib.call("skb_rowdot_gemv", f.LinvT, f.ld, m, m, 2, t, z, _Ptr(stop_ptr), sp_)
         _lib.call("skb_pcg_step_b", r, z, q, m, t_max, B.state, B.trace, sp_)
-    st = state_view[8:12].cpu().numpy()
+    st = to_host(state_view[8:12])
     iters, conv, status = int(st[2]), int(st[3]), int(st[1])
     n = iters + 1
-    B.trace_host[:n] = B.trace[:n].cpu().numpy()
+    B.trace_host[:n] = to_host(B.trace[:n])
     return iters, conv, status
 
 
 def _state_result(B):
-    st = B.state.view(torch.int32)[8:12].cpu().numpy()
+    st = to_host(B.state.view(torch.int32)[8:12])
     iters, conv, status = int(st[2]), int(st[3]), int(st[1])
-    B.trace_host[:iters + 1] = B.trace[:iters + 1].cpu().numpy()
+    B.trace_host[:iters + 1] = to_host(B.trace[:iters + 1])
     return iters, conv, status
 
 
@@ -173,7 +173,7 @@ def _apply_step(op, q, Aq, stop_ptr, state_view):
     if isinstance(op, NormalOperator):
         op.apply(q, out=Aq, gate=_Ptr(stop_ptr))
         return True
-    if int(state_view[8].item()):
+    if int(to_host(state_view[8:9])[0]):
         return False
     Aq.copy_(op.apply(q))
     return True
@@ -271,7 +271,7 @@ def direct_solve(op: "NormalOperator", p: torch.Tensor, cap: int = DIRECT_CAP) -
     _lib.call("skb_set_identity_pad", G, Mp, m, Mp, stream_ptr())
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.call("skb_potrf", G, Mp, Mp, status, ws, cap_b, stream_ptr())
-    if int(status.item()) & 4:
+    if int(to_host(status.reshape(-1)[:1])[0]) & 4:
         raise NotPositiveDefinite("Cholesky of the normal matrix failed")
     Linv = torch.empty_like(G)
     _lib.call("skb_trtri", G, Linv, Mp, Mp, ws, cap_b, stream_ptr())

@@ -23,7 +23,7 @@ from . import _lib
 from . import kernels as K
 from .distributed import MAX, MIN, SUM, Comm
 from .errors import DimensionMismatch, ZeroRow
-from .runtime import F64, require_cuda, stream_ptr, workspace
+from .runtime import F64, require_cuda, stream_ptr, to_host, workspace
 
 
 SPARSE_DENSITY = 0.1  # CSC device storage below this fill (12 B/nnz vs 8 B/entry dense)
@@ -241,7 +241,7 @@ class DeviceLP:
         out = reduce_call("skb_vec_stats", 4, a, sub, a.numel())
         if global_:
             self.comm.combine_(out, (SUM, SUM, MAX, MIN))
-        return out.detach().cpu().numpy()
+        return to_host(out)
 
     def norm_m(self, a, sub=None) -> float:
         """||a - sub|| of a replicated m-vector (no communication)."""

@@ -26,7 +26,7 @@ import torch
 from . import _lib
 from .errors import RankDeficient
 from .kernels import DeviceMatrix
-from .runtime import F64, stream_ptr, workspace
+from .runtime import F64, stream_ptr, to_host, workspace
 
 RANK_TOL = 1e-12
 
@@ -113,7 +113,7 @@ def _build_distributed(X: DeviceMatrix, rank_tol: float, sketch_tag) -> Precondi
     def chol(G):
         status.zero_()
         _lib.call("skb_potrf", G, Mp, Mp, status, ws, cap, stream_ptr())
-        return int(status.item())
+        return int(to_host(status.reshape(-1)[:1])[0])
 
     G = gram(X)
     shifted = False
@@ -121,7 +121,7 @@ def _build_distributed(X: DeviceMatrix, rank_tol: float, sketch_tag) -> Precondi
         shifted = True
         fro = (X.cols[:, :m] * X.cols[:, :m]).sum().reshape(1)
         comm.allreduce_(fro)
-        shift = 11.0 * (m * w_total + m * (m + 1)) * 1.1102230246251565e-16 * float(fro.item())
+        shift = 11.0 * (m * w_total + m * (m + 1)) * 1.1102230246251565e-16 * float(to_host(fro.reshape(-1)[:1])[0])
         G = gram(X)
         G.diagonal()[:m] += shift
         if chol(G) & 4:
@@ -146,7 +146,7 @@ def _build_distributed(X: DeviceMatrix, rank_tol: float, sketch_tag) -> Precondi
             L1i = Linv.clone()
     LinvT = torch.empty_like(Linv)
     _lib.call("skb_transpose", Linv, LinvT, Mp, Mp, stream_ptr())
-    dstat = torch.stack([dprod.min(), dprod.max()]).cpu().numpy()
+    dstat = to_host(torch.stack([dprod.min(), dprod.max()]))
     dmin, dmax = float(dstat[0]), float(dstat[1])
     if not (dmax > 0.0) or not np.isfinite(dmin) or dmin / dmax < rank_tol:
         raise RankDeficient(

@@ -69,6 +69,25 @@ class Scalars:
         return self.host.numpy().copy()
 
 
+_PIN = threading.local()
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """A small device tensor as a host numpy array, through the calling
+    thread's pinned staging buffer (a pageable readback costs several times
+    the latency, and the solver reads a few scalars back every step)."""
+    if not t.is_cuda:
+        return t.detach().numpy()
+    nbytes = t.numel() * t.element_size()
+    buf = getattr(_PIN, "buf", None)
+    if buf is None or buf.numel() < nbytes:
+        buf = _PIN.buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, pin_memory=True)
+    view = buf[:nbytes].view(t.dtype).view(t.shape)
+    view.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return view.numpy().copy()
+
+
 def lda_for(m: int) -> int:
     """Column stride of the device layout: even, so every column is 16-byte aligned."""
     return m + (m & 1)
