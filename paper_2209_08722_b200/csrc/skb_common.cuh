@@ -68,6 +68,27 @@ SKB_DEV uint64_t l2_evict_first_policy() {
   return pol;
 }
 
+// Read-only gathers that should not displace L2-resident working data:
+// no L1 allocation, L2 evict-first.
+SKB_DEV double ldg_ef(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+SKB_DEV int ldg_ef(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+SKB_DEV long long ldg_ef(const long long* p, uint64_t pol) {
+  long long v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;"
+               : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 // 1-D bulk async copy global -> shared (TMA engine, no tensor map), completes
 // as tx bytes on the mbarrier. dst/src 16-byte aligned, bytes % 16 == 0.
 SKB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {

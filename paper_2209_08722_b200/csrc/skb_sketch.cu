@@ -397,17 +397,23 @@ __global__ void __launch_bounds__(32)
 // scipy's (bit-exact); buckets are independent, so all w threads run at once
 // (a shared-memory m-vector per bucket would allow only ~2 buckets per SM at
 // m = 1e4). Index loads of the next member are issued ahead of the RMWs.
-constexpr int kRmwThreads = 128;
+constexpr int kRmwThreads = 256;
 constexpr int kRmwStage = 8;
 
+// (Development fallback, SKB_CSC_SKETCH_RMW=1: thread per bucket, or S threads
+// per bucket owning row slices; random HBM read-modify-writes of X, 27 ms at
+// c4 with s = 4 whatever S.)
+template <int S>
 __global__ void __launch_bounds__(kRmwThreads)
     csc_sketch_rmw_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
                           const double* __restrict__ av, const double* __restrict__ d,
                           const uint64_t* __restrict__ start, const int32_t* __restrict__ mem_e,
-                          const double* __restrict__ wvals, int s, int w,
+                          const double* __restrict__ wvals, int s, int w, int m,
                           double* __restrict__ X, int64_t ldx) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = (int)(gt / S), sl = (int)(gt % S);
   if (b >= w) return;
+  const int rlo = (int)((int64_t)m * sl / S), rhi = (int)((int64_t)m * (sl + 1) / S);
   double* __restrict__ Xb = X + (int64_t)b * ldx;
   const uint64_t e0 = start[b], e1 = start[b + 1];
   int64_t ei_next = e0 < e1 ? mem_e[e0] : 0;
@@ -423,12 +429,148 @@ __global__ void __launch_bounds__(kRmwThreads)
 #pragma unroll
       for (int q = 0; q < kRmwStage; ++q) {
         const bool ok = t0 + q < c1;
-        r[q] = ok ? rowidx[t0 + q] : 0;
+        r[q] = ok ? rowidx[t0 + q] : -1;
         a[q] = ok ? av[t0 + q] : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < kRmwStage; ++q)
-        if (t0 + q < c1) Xb[r[q]] = __dadd_rn(Xb[r[q]], __dmul_rn(__dmul_rn(a[q], dj), wv));
+        if (r[q] >= rlo && r[q] < rhi)
+          Xb[r[q]] = __dadd_rn(Xb[r[q]], __dmul_rn(__dmul_rn(a[q], dj), wv));
+    }
+  }
+}
+
+// Large m (c4: m = 1e4, w = 4e4, s = 4): a warp per bucket, the buckets in
+// flight limited to the resident warps (~1,200 x 80 KB bucket rows of X stay
+// in L2 while they are updated). The warp takes its members 32 at a time
+// (lane = member, ascending = the reference's order) through a 3-stage load
+// pipeline (member ids -> column meta -> the column's first kL2U row indices
+// and values), so every HBM gather is in flight one chunk ahead. A chunk's
+// entries are applied in parallel where their row is unique in the chunk (a
+// hashed per-warp count table); entries whose row may repeat are applied
+// lane by lane in ascending lane order. Each (bucket, row) sum thus runs in
+// ascending member order exactly as scipy's, and X is touched only in L2.
+constexpr int kL2Threads = 128, kL2U = 8, kL2Hash = 2048;
+
+struct L2Meta {  // one member's column: first entry, count, d_j and the sketch value
+  int64_t c0;
+  int nn;
+  double dj, wv;
+};
+
+__global__ void __launch_bounds__(kL2Threads)
+    csc_sketch_l2_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                         const double* __restrict__ av, const double* __restrict__ d,
+                         const uint64_t* __restrict__ start, const int32_t* __restrict__ mem_e,
+                         const double* __restrict__ wvals, int s, int w,
+                         double* __restrict__ X, int64_t ldx) {
+  __shared__ int cnt_all[(kL2Threads / 32) * kL2Hash];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int* cnt = cnt_all + wid * kL2Hash;
+  for (int i = lane; i < kL2Hash; i += 32) cnt[i] = 0;
+  __syncwarp();
+  const int gw = blockIdx.x * (kL2Threads / 32) + wid, nw = gridDim.x * (kL2Threads / 32);
+  const uint64_t pol = l2_evict_first_policy();  // gathers must not evict the X rows
+  for (int b = gw; b < w; b += nw) {
+    double* __restrict__ Xb = X + (int64_t)b * ldx;
+    const int64_t e0 = (int64_t)start[b], e1 = (int64_t)start[b + 1];
+    const int nchunk = (int)((e1 - e0 + 31) / 32);
+    // pipeline registers: ei (chunk k+2), meta (chunk k+1), entries (chunk k)
+    auto load_ei = [&](int k) -> int64_t {
+      const int64_t e = e0 + 32 * (int64_t)k + lane;
+      return (k < nchunk && e < e1) ? (int64_t)ldg_ef(&mem_e[e], pol) : -1;
+    };
+    auto load_meta = [&](int64_t ei) -> L2Meta {
+      L2Meta mt{0, 0, 0.0, 0.0};
+      if (ei >= 0) {
+        const int64_t j = ei / s;
+        mt.c0 = ldg_ef(reinterpret_cast<const long long*>(colptr) + j, pol);
+        mt.nn = (int)(ldg_ef(reinterpret_cast<const long long*>(colptr) + j + 1, pol) - mt.c0);
+        mt.dj = ldg_ef(&d[j], pol);
+        mt.wv = ldg_ef(&wvals[ei], pol);
+      }
+      return mt;
+    };
+    int rr[kL2U];
+    double aa[kL2U];
+    auto load_entries = [&](const L2Meta& mt) {
+#pragma unroll
+      for (int q = 0; q < kL2U; ++q) {
+        const bool ok = q < mt.nn;
+        rr[q] = ok ? ldg_ef(&rowidx[mt.c0 + q], pol) : -1;
+        aa[q] = ok ? ldg_ef(&av[mt.c0 + q], pol) : 0.0;
+      }
+    };
+    int64_t ei_next = load_ei(1);
+    L2Meta mt_cur = load_meta(load_ei(0));
+    L2Meta mt_next = load_meta(ei_next);
+    ei_next = load_ei(2);
+    load_entries(mt_cur);
+    for (int k = 0; k < nchunk; ++k) {
+      // values of chunk k (entries loaded one iteration ago)
+      int r[kL2U];
+      double v[kL2U];
+#pragma unroll
+      for (int q = 0; q < kL2U; ++q) {
+        r[q] = rr[q];
+        v[q] = __dmul_rn(__dmul_rn(aa[q], mt_cur.dj), mt_cur.wv);
+      }
+      const int nn = mt_cur.nn;
+      const int64_t c0 = mt_cur.c0;
+      const double dj = mt_cur.dj, wv = mt_cur.wv;
+      // keep the pipeline going: entries of chunk k+1, meta of chunk k+2, ids of k+3
+      mt_cur = mt_next;
+      load_entries(mt_cur);
+      mt_next = load_meta(ei_next);
+      ei_next = load_ei(k + 3);
+      const bool long_col = __any_sync(0xffffffffu, nn > kL2U);
+      if (!long_col) {
+#pragma unroll
+        for (int q = 0; q < kL2U; ++q)
+          if (q < nn) atomicAdd(&cnt[r[q] & (kL2Hash - 1)], 1);
+        __syncwarp();
+        bool uq[kL2U];
+        bool any_rep = false;
+#pragma unroll
+        for (int q = 0; q < kL2U; ++q) {
+          uq[q] = q < nn && cnt[r[q] & (kL2Hash - 1)] == 1;
+          any_rep |= q < nn && !uq[q];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < kL2U; ++q)
+          if (q < nn) cnt[r[q] & (kL2Hash - 1)] = 0;
+        // unique rows: all RMWs of the lane in flight together
+        double x[kL2U];
+#pragma unroll
+        for (int q = 0; q < kL2U; ++q) x[q] = uq[q] ? Xb[r[q]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kL2U; ++q)
+          if (uq[q]) Xb[r[q]] = __dadd_rn(x[q], v[q]);
+        // possibly repeated rows: lane by lane, ascending (= member order)
+        for (unsigned g = __ballot_sync(0xffffffffu, any_rep); g; g &= g - 1) {
+          if (__ffs(g) - 1 == lane) {
+#pragma unroll
+            for (int q = 0; q < kL2U; ++q)
+              if (q < nn && !uq[q]) Xb[r[q]] = __dadd_rn(Xb[r[q]], v[q]);
+          }
+          __syncwarp();
+        }
+        __syncwarp();
+      } else {
+        // a column longer than kL2U in this chunk: the whole chunk lane by lane
+        for (int l = 0; l < 32; ++l) {
+          if (l == lane) {
+            for (int q = 0; q < nn; ++q) {
+              const int rq = q < kL2U ? r[q] : __ldg(&rowidx[c0 + q]);
+              const double vq =
+                  q < kL2U ? v[q] : __dmul_rn(__dmul_rn(__ldg(&av[c0 + q]), dj), wv);
+              Xb[rq] = __dadd_rn(Xb[rq], vq);
+            }
+          }
+          __syncwarp();
+        }
+      }
     }
   }
 }
@@ -446,10 +588,19 @@ extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx
   unsigned int* counter;
   int rc = bucket_sort(cols, n, s, w, &ws, st, &start, &mem_e, &counter);
   if (rc) return rc;
+  if (m > 2048 && !getenv("SKB_CSC_SKETCH_RMW")) {
+    cudaMemsetAsync(X, 0, (size_t)w * ldx * 8, st);
+    static const int l2cps = getenv("SKB_L2_CPS") ? atoi(getenv("SKB_L2_CPS")) : 2;
+    const int grid = std::min(skb_num_sms() * l2cps, (int)((w + 3) / 4));
+    csc_sketch_l2_kernel<<<grid, kL2Threads, 0, st>>>(colptr, rowidx, av, d, start, mem_e, vals,
+                                                      s, w, X, ldx);
+    return skb_launch_status(__func__);
+  }
   if (m > 2048) {
     cudaMemsetAsync(X, 0, (size_t)w * ldx * 8, st);
-    csc_sketch_rmw_kernel<<<(w + kRmwThreads - 1) / kRmwThreads, kRmwThreads, 0, st>>>(
-        colptr, rowidx, av, d, start, mem_e, vals, s, w, X, ldx);
+    csc_sketch_rmw_kernel<1><<<(unsigned)((w + kRmwThreads - 1) / kRmwThreads), kRmwThreads, 0,
+                               st>>>(colptr, rowidx, av, d, start, mem_e, vals, s, w, (int)m, X,
+                                     ldx);
     return skb_launch_status(__func__);
   }
   const size_t smem = (size_t)m * 8 + 32 * kCscStage * 4 + 32 * 4 + 16 + 32 * kCscStage * 8;

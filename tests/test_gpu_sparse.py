@@ -89,6 +89,24 @@ def test_csc_sketch_apply_bit_exact(K):
     assert np.array_equal(_h(X.cols)[:, :3000].T, ref)
 
 
+@pytest.mark.parametrize("m,n,k,w,s", [(2500, 10_000, 5, 600, 4), (2600, 8000, 12, 500, 3)])
+def test_csc_sketch_large_m_bit_exact(K, m, n, k, w, s):
+    """m > 2048 takes the warp-per-bucket L2 kernel: few buckets (many repeated
+    rows per member chunk -> the ordered path) and columns longer than its
+    8-entry register window (k = 12 -> the lane-by-lane path), bit-exact
+    against the C restatement of scipy's summation order."""
+    from paper_2209_08722_b200 import sketching as S
+    from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
+    lpd = sparse_wide_lp(m, n, k, m + k)
+    lp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c))
+    d = 10.0 ** np.random.Generator(np.random.Philox(m)).uniform(-3, 3, lpd.n)
+    W = S.build_sparse_embedding(lpd.n, w, s, 90 + k)
+    X = S.apply_sketch(lp, _t(d), W)
+    cols, vals = O.sparse_embedding(lpd.n, w, s, 90 + k)
+    ref = chash.adw_dense(lpd.A.toarray(), d, cols, vals, w)
+    assert np.array_equal(_h(X.cols)[:, :m].T, ref)
+
+
 def test_sparse_trajectory_s4(K, monkeypatch):
     from paper_2209_08722_b200 import ipm_core as IC
     from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
