@@ -215,14 +215,17 @@ int skb_factor_cholqr2(const double* X, int64_t ldx, int32_t w, int32_t m, doubl
                        double* LinvT, double* Lfac, double* stats_host, void* workspace,
                        size_t ws_bytes, void* stream);
 
-/* C = alpha op(A) op(B) + beta C (row-major, FP64 DMMA tensor cores, batched). */
+/* C = alpha op(A) op(B) + beta C (row-major, FP64 DMMA tensor cores, batched).
+ * The GEMM-class work of the reference's LAPACK gesdd / numpy matmul
+ * (preconditioning.py:46, sketching.py:158-159, krylov_solvers.py:50). */
 int skb_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, double alpha,
              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
              int64_t ldc, int32_t lower_only, int32_t batch, int64_t strideA, int64_t strideB,
              int64_t strideC, void* workspace, size_t ws_bytes, void* stream);
 
 /* The same product emulated in FP64 on the INT8 tensor cores (CRT over 16
- * moduli, csrc/skb_ozaki.cu); lower_only writes j <= i only. skb_gemm routes
+ * moduli, csrc/skb_ozaki.cu; the same reference seams as skb_gemm, results
+ * within fp64 rounding of them); lower_only writes j <= i only. skb_gemm routes
  * large unbatched products here (SKB_GEMM_EMU=0 disables). Returns
  * SKB_ERR_UNSUPPORTED when cuBLASLt cannot be loaded or the workspace is short. */
 int skb_gemm_ozaki(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, double alpha,
