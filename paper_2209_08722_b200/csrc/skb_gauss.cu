@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(kZThreads, 3)
                     double sqrtw, double* __restrict__ out) {
   __shared__ ZigTables T;
   __shared__ uint32_t warp_sum[2][kZThreads / 32];
+  __shared__ double wbuf[kZThreads / 32][32 * kZPer];
   zig_load_tables(&T);
   const double rsqrtw = __drcp_rn(sqrtw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -372,26 +373,34 @@ __global__ void __launch_bounds__(kZThreads, 3)
     for (int w2 = 0; w2 < kZThreads / 32; ++w2)
       if (w2 < warp) wbase += warp_sum[par][w2];
     const uint64_t first = base + wbase + incl - c;  // global index of this thread's first draw
+    // the warp's draws are one contiguous range: stage them in shared memory
+    // and store coalesced (direct per-thread stores touch 32 lines per instruction)
+    const uint64_t wfirst = __shfl_sync(0xffffffffu, first, 0);
+    const uint32_t wcount = __shfl_sync(0xffffffffu, incl, 31);
+    double* buf = wbuf[warp];
+    const uint32_t off = (uint32_t)(first - wfirst);
 #pragma unroll
     for (int i = 0, k = 0; i < kZPer; ++i) {
       if (outm & (1u << i)) {
-        const uint64_t idx = first + k;
-        if (!((ac >> i) & 1u) && idx >= lo && idx < need)
-          out[idx - lo] = div_by(vv[i], sqrtw, rsqrtw);
+        if (!((ac >> i) & 1u)) buf[off + k] = div_by(vv[i], sqrtw, rsqrtw);
         ++k;
       }
     }
     // accepted slow attempts (rare): recompute their values in a rolled loop
     for (uint32_t rest = ac; rest; rest &= rest - 1) {
       const int i = __ffs(rest) - 1;
-      const uint64_t idx = first + __popc(outm & ((1u << i) - 1u));
-      if (idx < lo || idx >= need) continue;
       const uint64_t q = my0 + i;
       double v;
       int len;
       zig_slow(T, k0, k1, q, out64(k0, k1, q), &v, &len);
-      out[idx - lo] = div_by(v, sqrtw, rsqrtw);
+      buf[off + __popc(outm & ((1u << i) - 1u))] = div_by(v, sqrtw, rsqrtw);
     }
+    __syncwarp();
+    for (uint32_t p = lane; p < wcount; p += 32) {
+      const uint64_t idx = wfirst + p;
+      if (idx >= lo && idx < need) out[idx - lo] = buf[p];
+    }
+    __syncwarp();
   }
 }
 
