@@ -530,9 +530,24 @@ size_t skb_oz_bytes(int M, int N, int K, bool share) {
 
 static std::atomic<long long> g_calls{0};
 
+// K = 0: C = beta C (the empty product), on the written part only.
+__global__ void scale_c_kernel(double* C, int64_t ldc, int M, int N, int lower_only, double beta) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)M * N) return;
+  const int i = (int)(e / N), j = (int)(e % N);
+  if (lower_only && j > i) return;
+  double* p = C + (int64_t)i * ldc + j;
+  *p = beta == 0.0 ? 0.0 : beta * *p;
+}
+
 int skb_oz_gemm(const skb_oz_args& g, skb_ws* ws, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return 0;
-  if (g.K <= 0) return 1;
+  if (g.K <= 0) {
+    const int64_t tot = (int64_t)g.M * g.N;
+    scale_c_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g.C, g.ldc, g.M, g.N,
+                                                                 g.lower_only, g.beta);
+    return skb_launch_status("ozaki k=0");
+  }
   if (!oz::lt().ok) return 1;
   // K chunk: <= kMaxK (exact INT32 sums) and small enough that both residue
   // sets plus a 1024-row INT32 slab fit the workspace; chunks accumulate in fp64.

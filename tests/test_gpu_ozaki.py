@@ -121,3 +121,30 @@ def test_skb_gemm_routes_large_products(L, monkeypatch):
     scale = np.abs(ref).max()
     assert np.max(np.abs(outs["2"] - np.tril(ref))) <= 1e-13 * scale
     assert np.max(np.abs(outs["2"] - outs["0"])) <= 1e-13 * scale
+
+
+def test_ozaki_nonfinite_rows_and_empty_k(L):
+    """A NaN / inf in an operand row poisons only that output row (NaN), as in
+    fp64; K = 0 gives beta C."""
+    from paper_2209_08722_b200.runtime import stream_ptr, workspace
+    g = np.random.Generator(np.random.Philox(21))
+    M, N, K = 64, 48, 700
+    A = g.standard_normal((M, K))
+    B = g.standard_normal((K, N))
+    A[3, 10] = np.nan
+    A[7, 0] = np.inf
+    C = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    ws, cap = workspace(int(L.lib().skb_gemm_ozaki_workspace_bytes(M, N, K)))
+    L.call("skb_gemm_ozaki", 0, 0, M, N, K, 1.0, _t(A), K, _t(B), N, 0.0, C, N, 0, ws, cap,
+           stream_ptr())
+    out = C.cpu().numpy()
+    assert np.isnan(out[3]).all() and np.isnan(out[7]).all()
+    ok = np.ones(M, bool)
+    ok[[3, 7]] = False
+    ref = _exact(A[ok], B)
+    assert np.all(np.abs(out[ok] - ref).astype(np.float64) <= _bound(A[ok], B) + 1e-300)
+    C0 = g.standard_normal((M, N))
+    Cd = _t(C0)
+    L.call("skb_gemm_ozaki", 0, 0, M, N, 0, 1.0, _t(A), K, _t(B), N, 0.5, Cd, N, 0, ws, cap,
+           stream_ptr())
+    assert np.array_equal(Cd.cpu().numpy(), 0.5 * C0)
