@@ -18,6 +18,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cub/device/device_histogram.cuh>
+#include <cub/device/device_radix_sort.cuh>
+
 #include "skb_common.cuh"
 #include "skb_internal.h"
 
@@ -282,11 +285,65 @@ __global__ void sketch_gather_kernel(const int32_t* __restrict__ cols,
 
 using namespace skb;
 
+namespace skb {
+__global__ void iota_kernel(int32_t* __restrict__ v, int64_t N) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) v[i] = (int32_t)i;
+}
+}  // namespace skb
+
+// Large N: stable LSD radix sort (CUB) of the entries by bucket, ceil(log2 w)
+// key bits; stability keeps ascending entry order inside each bucket, so the
+// result equals the counting sort's.
+constexpr int64_t kRadixMinN = 1ll << 24;
+
+static size_t radix_temp_bytes(int64_t N, int32_t w) {
+  size_t sort_b = 0, hist_b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)N, 0, 32);
+  cub::DeviceHistogram::HistogramEven(nullptr, hist_b, (const int32_t*)nullptr,
+                                      (uint32_t*)nullptr, (int)w + 1, 0, (int)w, (int)N);
+  return std::max(sort_b, hist_b) + 256;
+}
+
 extern "C" size_t skb_sketch_workspace_bytes(int64_t n, int32_t w, int32_t s) {
   const int64_t N = n * (int64_t)s;
   int64_t C = std::max<int64_t>(4096, (N * (int64_t)w) / (16ll << 20) + 1);
   const int64_t nch = (N + C - 1) / C;
-  return (size_t)nch * w * 4 + (size_t)w * 4 + (size_t)(w + 1) * 8 + (size_t)N * 4 + 16 + 8 * 256;
+  const size_t counting =
+      (size_t)nch * w * 4 + (size_t)w * 4 + (size_t)(w + 1) * 8 + (size_t)N * 4 + 16 + 8 * 256;
+  if (N < kRadixMinN && !getenv("SKB_BUCKET_RADIX")) return counting;
+  const size_t radix = (size_t)w * 4 + (size_t)(w + 1) * 8 + (size_t)N * 4 * 3 + 16 +
+                       radix_temp_bytes(N, w) + 8 * 256;
+  return std::max(counting, radix);
+}
+
+static int bucket_sort_radix(const int32_t* cols, int64_t N, int32_t w, skb_ws* ws,
+                             cudaStream_t st, uint64_t** start_out, int32_t** mem_out,
+                             unsigned int** counter_out) {
+  uint32_t* total = (uint32_t*)skb_ws_take(ws, (size_t)w * 4);
+  uint64_t* start = (uint64_t*)skb_ws_take(ws, (size_t)(w + 1) * 8);
+  int32_t* mem_e = (int32_t*)skb_ws_take(ws, (size_t)N * 4);
+  uint32_t* keys = (uint32_t*)skb_ws_take(ws, (size_t)N * 4);
+  int32_t* iota = (int32_t*)skb_ws_take(ws, (size_t)N * 4);
+  unsigned int* counter = (unsigned int*)skb_ws_take(ws, 16);
+  const size_t tb = radix_temp_bytes(N, w);
+  void* tmp = skb_ws_take(ws, tb);
+  if (!total || !start || !mem_e || !keys || !iota || !counter || !tmp) return SKB_ERR_WORKSPACE;
+  cudaMemsetAsync(counter, 0, 16, st);
+  int bits = 1;
+  while ((1ll << bits) < (int64_t)w) ++bits;
+  size_t b1 = tb;
+  cub::DeviceHistogram::HistogramEven(tmp, b1, cols, total, (int)w + 1, 0, (int)w, (int)N, st);
+  scan_buckets_kernel<<<1, 1024, 0, st>>>(total, start, w);
+  iota_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(iota, N);
+  size_t b2 = tb;
+  cub::DeviceRadixSort::SortPairs(tmp, b2, reinterpret_cast<const uint32_t*>(cols), keys, iota,
+                                  mem_e, (int)N, 0, bits, st);
+  *start_out = start;
+  *mem_out = mem_e;
+  *counter_out = counter;
+  return skb_launch_status("bucket_sort_radix");
 }
 
 // Stable counting sort of the n*s hash entries by bucket -> start[w+1], mem_e[N]
@@ -295,6 +352,9 @@ static int bucket_sort(const int32_t* cols, int64_t n, int32_t s, int32_t w, skb
                        cudaStream_t st, uint64_t** start_out, int32_t** mem_out,
                        unsigned int** counter_out) {
   const int64_t N = n * (int64_t)s;
+  if ((N >= kRadixMinN || getenv("SKB_BUCKET_RADIX")) && N < (1ll << 31) &&
+      !getenv("SKB_BUCKET_COUNTING"))
+    return bucket_sort_radix(cols, N, w, ws, st, start_out, mem_out, counter_out);
   const int64_t C = std::max<int64_t>(4096, (N * (int64_t)w) / (16ll << 20) + 1);
   const int64_t nch = (N + C - 1) / C;
   int32_t* hist = (int32_t*)skb_ws_take(ws, (size_t)nch * w * 4);

@@ -62,8 +62,10 @@ def test_sketch_apply_golden_bits(P):
                                      (37, 5000, 300, 2), (1000, 20_000, 4000, 1),
                                      (700, 8000, 2000, 3), (2000, 6000, 4000, 1),
                                      (3000, 4000, 3500, 2), (1000, 30_000, 4000, 4)])
-def test_sketch_apply_bit_exact_vs_c_oracle(P, m, n, w, s):
+def test_sketch_apply_bit_exact_vs_c_oracle(P, monkeypatch, m, n, w, s):
     from paper_2209_08722_b200 import sketching as S
+    if s == 4:  # the radix-sort bucket order (used from 2^24 entries) on the s = 4 cases
+        monkeypatch.setenv("SKB_BUCKET_RADIX", "1")
     g = np.random.Generator(np.random.Philox(m + n))
     A = g.standard_normal((m, n))
     d = 10.0 ** g.uniform(-3, 3, n)

@@ -89,14 +89,20 @@ def test_csc_sketch_apply_bit_exact(K):
     assert np.array_equal(_h(X.cols)[:, :3000].T, ref)
 
 
-@pytest.mark.parametrize("m,n,k,w,s", [(2500, 10_000, 5, 600, 4), (2600, 8000, 12, 500, 3)])
-def test_csc_sketch_large_m_bit_exact(K, m, n, k, w, s):
+@pytest.mark.parametrize("m,n,k,w,s,radix", [(2500, 10_000, 5, 600, 4, False),
+                                              (2600, 8000, 12, 500, 3, False),
+                                              (2500, 10_000, 5, 600, 4, True)])
+def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix):
     """m > 2048 takes the warp-per-bucket L2 kernel: few buckets (many repeated
     rows per member chunk -> the ordered path) and columns longer than its
     8-entry register window (k = 12 -> the lane-by-lane path), bit-exact
-    against the C restatement of scipy's summation order."""
+    against the C restatement of scipy's summation order. radix: the bucket
+    order from the CUB radix sort (used from 2^24 entries) instead of the
+    counting sort."""
     from paper_2209_08722_b200 import sketching as S
     from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
+    if radix:
+        monkeypatch.setenv("SKB_BUCKET_RADIX", "1")
     lpd = sparse_wide_lp(m, n, k, m + k)
     lp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c))
     d = 10.0 ** np.random.Generator(np.random.Philox(m)).uniform(-3, 3, lpd.n)
