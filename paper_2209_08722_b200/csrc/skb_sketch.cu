@@ -292,10 +292,10 @@ __global__ void iota_kernel(int32_t* __restrict__ v, int64_t N) {
 }
 }  // namespace skb
 
-// Large N: stable LSD radix sort (CUB) of the entries by bucket, ceil(log2 w)
+// N >= 2^20: stable LSD radix sort (CUB) of the entries by bucket, ceil(log2 w)
 // key bits; stability keeps ascending entry order inside each bucket, so the
 // result equals the counting sort's.
-constexpr int64_t kRadixMinN = 1ll << 24;
+constexpr int64_t kRadixMinN = 1ll << 20;
 
 static size_t radix_temp_bytes(int64_t N, int32_t w) {
   size_t sort_b = 0, hist_b = 0;

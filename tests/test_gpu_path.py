@@ -64,7 +64,7 @@ def test_sketch_apply_golden_bits(P):
                                      (3000, 4000, 3500, 2), (1000, 30_000, 4000, 4)])
 def test_sketch_apply_bit_exact_vs_c_oracle(P, monkeypatch, m, n, w, s):
     from paper_2209_08722_b200 import sketching as S
-    if s == 4:  # the radix-sort bucket order (used from 2^24 entries) on the s = 4 cases
+    if s == 4:  # the radix-sort bucket order (default from 2^20 entries) on the s = 4 cases
         monkeypatch.setenv("SKB_BUCKET_RADIX", "1")
     g = np.random.Generator(np.random.Philox(m + n))
     A = g.standard_normal((m, n))
