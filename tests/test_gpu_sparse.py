@@ -97,8 +97,8 @@ def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix):
     rows per member chunk -> the ordered path) and columns longer than its
     8-entry register window (k = 12 -> the lane-by-lane path), bit-exact
     against the C restatement of scipy's summation order. radix: the bucket
-    order from the CUB radix sort (forced below its 2^20-entry threshold) instead of the
-    counting sort; default from 2^20 entries)."""
+    order from the CUB radix sort (its default from 2^20 entries, forced here)
+    instead of the counting sort."""
     from paper_2209_08722_b200 import sketching as S
     from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
     if radix:
