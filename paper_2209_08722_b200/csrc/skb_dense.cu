@@ -678,10 +678,12 @@ using namespace skb;
 // plus the HBM passes of the residue split and the CRT, against DMMA at
 // ~30 TFLOP/s on the (triangle-trimmed) flops. SKB_GEMM_EMU=0 disables it,
 // SKB_GEMM_EMU=2 forces it for every eligible shape (tests).
+static int emulate_one(const GemmArgs& g, skb_ws* ws, cudaStream_t st);
+
 static int try_emulated(const GemmArgs& g, int nbatch, skb_ws* ws, cudaStream_t st) {
   const char* env = getenv("SKB_GEMM_EMU");
   const int mode = env ? atoi(env) : 1;
-  if (!mode || nbatch != 1 || g.K < 256) return 1;
+  if (!mode || g.K < 256) return 1;
   const double M = g.M, N = g.N, K = g.K;
   double dm = 2.0 * M * N * K;
   if (g.lower_only) dm *= 0.5;
@@ -691,6 +693,19 @@ static int try_emulated(const GemmArgs& g, int nbatch, skb_ws* ws, cudaStream_t 
   const double t_emu = 16.0 * 1.1 * dm / 2.4e15 + ((M + N) * K * 26.0 + M * N * 80.0) / 5e12 +
                        60e-6;
   if (mode == 1 && !(t_emu < 0.8 * t_dmma)) return 1;
+  // batched (the triangular-inverse levels): one emulated product per item
+  for (int bi = 0; bi < nbatch; ++bi) {
+    GemmArgs gb = g;
+    gb.A = g.A + (int64_t)bi * g.sA;
+    gb.B = g.B + (int64_t)bi * g.sB;
+    gb.C = g.C + (int64_t)bi * g.sC;
+    const int rc = emulate_one(gb, ws, st);
+    if (rc) return bi == 0 ? rc : (rc == 1 ? SKB_ERR_WORKSPACE : rc);
+  }
+  return 0;
+}
+
+static int emulate_one(const GemmArgs& g, skb_ws* ws, cudaStream_t st) {
   skb_oz_args o{};
   o.a = g.ta ? skb_oz_operand{g.A, 1, g.lda} : skb_oz_operand{g.A, g.lda, 1};
   o.b = g.tb ? skb_oz_operand{g.B, g.ldb, 1} : skb_oz_operand{g.B, 1, g.ldb};

@@ -465,8 +465,11 @@ static int chunk(const skb_oz_args& g, int k0, int Kc, double beta, skb_ws* ws, 
   auto prep = [&](const double* p0, int64_t sr, int64_t sk, int R, int Rp, const double* kk,
                   int tri, unsigned long long* am, double2* mul, double* inv, int8_t* o) {
     cudaMemsetAsync(am, 0, (size_t)Rp * 8, st);
-    const int kchunk = 4096;
-    dim3 gm(sk == 1 ? (R + 7) / 8 : (R + 31) / 32, (Kc + kchunk - 1) / kchunk);
+    // k split so the grid covers the GPU ~4x (row blocks alone are too few at m ~ 2e3)
+    const int rb = sk == 1 ? (R + 7) / 8 : (R + 31) / 32;
+    const int want = std::max(1, (4 * skb_num_sms() + rb - 1) / rb);
+    const int kchunk = std::max(256, (int)up((Kc + want - 1) / want, 256));
+    dim3 gm(rb, (Kc + kchunk - 1) / kchunk);
     rowmax_kernel<<<gm, 256, 0, st>>>(p0, sr, sk, R, Kc, kk, kchunk, tri, k0, am);
     scales_kernel<<<(Rp + 255) / 256, 256, 0, st>>>(am, R, Rp, mul, inv);
     dim3 gs((unsigned)((Kp + kST - 1) / kST), (unsigned)((Rp + kST - 1) / kST));

@@ -13,7 +13,7 @@ def ev(fn, reps=50):
     for _ in range(reps): fn()
     b.record(); b.synchronize(); return a.elapsed_time(b) / reps * 1e3
 
-for Mp in (64, 128, 256, 1024, 2048):
+for Mp in [int(v) for v in os.environ.get("PROF_MPS", "64,128,256,1024,2048").split(",")]:
     g = torch.Generator(device="cuda"); g.manual_seed(0)
     X = torch.randn((4 * Mp, Mp), dtype=torch.float64, device="cuda", generator=g)
     spd = (X.t() @ X).contiguous()
