@@ -1,6 +1,7 @@
 """Summarise an ncu --csv launch list (gpu__time_duration.sum) by kernel, in launch order."""
 import csv, collections, sys
-rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+lines = [ln for ln in open(sys.argv[1]) if ln.startswith('"')]  # skip program output
+rows = [r for r in csv.reader(lines) if len(r) > 10]
 hdr = rows[0]; ki = hdr.index("Kernel Name"); vi = hdr.index("Metric Value")
 agg = collections.OrderedDict(); tot = 0.0
 for r in rows[1:]:
