@@ -895,17 +895,19 @@ static int potrf(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStr
 
 static int trtri(const double* L, double* Li, int64_t ld, int Mp, skb_ws* ws, cudaStream_t st);
 
-// Large Mp: two-level blocking. NBO-wide outer panels (512 / 1024 / 2048 as
-// Mp grows): the diagonal block is factored by potrf (64-wide panels) and
+// Large Mp: two-level blocking. NBO-wide outer panels: the diagonal block is
+// factored by potrf (64-wide panels) and
 // inverted by trtri, the panel L21 = A21 L11^-T is ONE NBO-deep GEMM into a
 // scratch block, and the trailing update A22 -= L21 L21' ONE lower-tile SYRK.
 // A few large GEMMs per NBO columns instead of NBO/64 small ones; from
 // NBO = 1024 they are long enough for the INT8 emulation's cost model.
-static int outer_block(int Mp) { return Mp >= 8192 ? 2048 : (Mp >= 4096 ? 1024 : 512); }
+// (measured at Mp = 2048..10048: the plain 64-panel loop wins below ~6000,
+// 2048-wide outer blocks above)
+constexpr int kNBO = 2048, kPotrfBigMin = 6144;
 
 static int potrf_big(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStream_t st) {
-  if (Mp < 2048) return potrf(G, ld, Mp, status, ws, st);
-  const int NBO = outer_block(Mp);
+  if (Mp < kPotrfBigMin) return potrf(G, ld, Mp, status, ws, st);
+  const int NBO = kNBO;
   const size_t mark = ws->off;
   double* Lc = (double*)skb_ws_take(ws, (size_t)NBO * NBO * 8);
   double* Lci = (double*)skb_ws_take(ws, (size_t)NBO * NBO * 8);
