@@ -235,6 +235,23 @@ int skb_gemm_ozaki(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, doub
 size_t skb_gemm_ozaki_workspace_bytes(int32_t M, int32_t N, int32_t K);
 int64_t skb_gemm_ozaki_calls(void);
 
+/* One-shot all-reduce of an m-vector over NVLink peer memory (csrc/skb_p2p.cu):
+ * the exchange SURVEY.md §8(e) puts after every sharded A-pass that yields an
+ * m-vector (reference: the single-process sums of krylov_solvers.py:46-47,
+ * ipm_core.py:196-242). Peers' symmetric buffers ([2][ld] doubles) and flag
+ * words (>= skb_p2p_max_blocks(m) u64) are opened with skb_ipc_open; mode 0 =
+ * publish + gather, 1 / 2 = one half (single-process tests). */
+int skb_p2p_alloc(int64_t bytes, uint64_t* dev_ptr_out);
+int skb_p2p_free(uint64_t dev_ptr);
+int skb_ipc_handle(void* dev_ptr, void* handle_out);
+int skb_ipc_open(const void* handle, uint64_t* dev_ptr_out);
+int skb_ipc_close(uint64_t dev_ptr);
+int32_t skb_p2p_can_access(int32_t device, int32_t peer);
+int32_t skb_p2p_max_blocks(int64_t m);
+int skb_p2p_allreduce(const double* local, double* out, int64_t m, int64_t ld, int32_t rank,
+                      int32_t world, const uint64_t* data_ptrs, const uint64_t* flag_ptrs,
+                      uint64_t epoch, int32_t mode, int* err, void* stream);
+
 /* Blocked Cholesky (lower, in place) and triangular inverse; Mp % 64 == 0.
  * status: device int, SKB_ST_CHOL_FAIL on a nonpositive pivot. */
 int skb_potrf(double* G, int64_t ld, int32_t Mp, int* status, void* workspace, size_t ws_bytes,

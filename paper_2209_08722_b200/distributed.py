@@ -22,10 +22,87 @@ except Exception:  # pragma: no cover
 SUM, MAX, MIN = "sum", "max", "min"
 
 
+class P2PAllreduce:
+    """One-shot all-reduce of m-vectors over NVLink peer memory
+    (csrc/skb_p2p.cu): symmetric buffers from cudaMalloc, opened by every peer
+    through CUDA IPC; one kernel per all-reduce (publish, acquire the peers'
+    flags, sum in rank order), no NCCL call on the per-pass path. Comm builds
+    it collectively on the first eligible all-reduce, in phases that every rank
+    agrees on before the next collective (so a local failure cannot leave a
+    peer blocked), and checks it against NCCL once."""
+
+    def __init__(self, comm: "Comm", cap: int):
+        self.comm, self.rank, self.world = comm, comm.rank, comm.world
+        self.ld = cap + (cap & 1)
+        self.cap = cap
+        self.epoch = 0
+        self.err = None
+        self._own = None
+        self._opened = []
+        self.data_ptrs = self.flag_ptrs = None
+
+    def alloc_local(self):
+        """Phase A (local): own buffers and their IPC handles (128 bytes)."""
+        import numpy as np
+        from . import _lib
+        nb = int(_lib.lib().skb_p2p_max_blocks(self.cap))
+        own = np.zeros(2, dtype=np.uint64)
+        _lib.call("skb_p2p_alloc", 16 * self.ld, own[0:].ctypes.data)
+        _lib.call("skb_p2p_alloc", 8 * max(nb, 1), own[1:].ctypes.data)
+        self._own = own
+        h = np.zeros(128, dtype=np.uint8)
+        _lib.call("skb_ipc_handle", int(own[0]), h[:64].ctypes.data)
+        _lib.call("skb_ipc_handle", int(own[1]), h[64:].ctypes.data)
+        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        return h
+
+    def open_peers(self, handles):
+        """Phase C (local): open every peer's buffers from the gathered handles."""
+        import numpy as np
+        from . import _lib
+        self.data_ptrs = np.zeros(self.world, dtype=np.uint64)
+        self.flag_ptrs = np.zeros(self.world, dtype=np.uint64)
+        for g, hb in enumerate(handles):
+            if g == self.rank:
+                self.data_ptrs[g], self.flag_ptrs[g] = self._own[0], self._own[1]
+                continue
+            p = np.zeros(2, dtype=np.uint64)
+            _lib.call("skb_ipc_open", hb[:64].ctypes.data, p[0:].ctypes.data)
+            self._opened.append(int(p[0]))
+            _lib.call("skb_ipc_open", hb[64:].ctypes.data, p[1:].ctypes.data)
+            self._opened.append(int(p[1]))
+            self.data_ptrs[g], self.flag_ptrs[g] = p[0], p[1]
+
+    def release(self):
+        from . import _lib
+        for p in self._opened:
+            try:
+                _lib.call("skb_ipc_close", p)
+            except Exception:
+                pass
+        self._opened = []
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        from . import _lib
+        from .runtime import stream_ptr
+        self.epoch += 1
+        _lib.call("skb_p2p_allreduce", t, t, t.numel(), self.ld, self.rank, self.world,
+                  self.data_ptrs.ctypes.data, self.flag_ptrs.ctypes.data, self.epoch, 0,
+                  self.err, stream_ptr())
+        return t
+
+
+def _p2p_enabled_env() -> bool:
+    import os
+    return os.environ.get("SKB_P2P", "1") != "0"
+
+
 class Comm:
     def __init__(self, group=None):
         self.group = group
         self.host_staging = False
+        self._p2p = None          # P2PAllreduce once built
+        self._p2p_state = None    # None: not tried, False: unavailable
         if dist is not None and dist.is_available() and dist.is_initialized():
             self.rank = dist.get_rank(group)
             self.world = dist.get_world_size(group)
@@ -42,8 +119,77 @@ class Comm:
         """Balanced contiguous column range [j0, j1) of this rank."""
         return shard_range(n, self.rank, self.world)
 
+    def _p2p_for(self, t: torch.Tensor):
+        """The NVLink all-reduce for a float64 CUDA m-vector, built (collectively,
+        on the first eligible call every rank makes with the same size) and
+        checked against NCCL once; None where it does not apply."""
+        if self._p2p_state is False or self.host_staging or not t.is_cuda:
+            return None
+        if t.dtype != torch.float64 or t.dim() != 1 or not t.is_contiguous():
+            return None
+        if self._p2p is not None:
+            return self._p2p if t.numel() <= self._p2p.cap else None
+        if not _p2p_enabled_env() or not (2 <= self.world <= 8):
+            self._p2p_state = False
+            return None
+        if t.numel() > (1 << 17):  # m-vectors only (every rank sees the same sizes)
+            return None
+        from . import _lib
+        dev_t = t.device
+        ok = torch.ones(1, dtype=torch.float64, device=dev_t)
+
+        def agree(flag: bool) -> bool:  # every rank learns whether all succeeded
+            ok.fill_(1.0 if flag else 0.0)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+            return ok.item() == 1.0
+
+        p2p = P2PAllreduce(self, max(t.numel(), 16384))
+        h = None
+        try:  # phase A (local): peer access to every rank's GPU, own buffers
+            dev = torch.cuda.current_device()
+            ids = [torch.zeros(1, dtype=torch.int64, device=dev_t) for _ in range(self.world)]
+            dist.all_gather(ids, torch.tensor([dev], dtype=torch.int64, device=dev_t),
+                            group=self.group)
+            if all(_lib.lib().skb_p2p_can_access(dev, int(i.item())) for i in ids):
+                h = p2p.alloc_local()
+        except Exception:
+            h = None
+        if not agree(h is not None):
+            self._p2p_state = False
+            return None
+        # phase B (collective): gather the handles
+        ht = torch.from_numpy(h).to(dev_t)
+        hs = [torch.empty_like(ht) for _ in range(self.world)]
+        dist.all_gather(hs, ht, group=self.group)
+        good = True
+        try:  # phase C (local): open the peers' buffers
+            p2p.open_peers([x.cpu().numpy() for x in hs])
+        except Exception:
+            good = False
+        if agree(good):
+            # phase D: one all-reduce checked against NCCL (a peer that never
+            # arrives makes the kernel time out to NaN, never hang)
+            g = torch.Generator(device=dev_t)
+            g.manual_seed(1234 + self.rank)
+            x = torch.randn(t.numel(), dtype=torch.float64, device=dev_t, generator=g)
+            y = x.clone()
+            p2p.allreduce_(x)
+            dist.all_reduce(y, group=self.group)
+            good = bool(torch.allclose(x, y, rtol=1e-12, atol=1e-12)) and \
+                int(p2p.err.item()) == 0
+            if agree(good):
+                self._p2p, self._p2p_state = p2p, True
+                return p2p
+        p2p.release()
+        self._p2p_state = False
+        return None
+
     def allreduce_(self, t: torch.Tensor, op: str = SUM) -> torch.Tensor:
         if self.world > 1:
+            if op == SUM:
+                p2p = self._p2p_for(t)
+                if p2p is not None:
+                    return p2p.allreduce_(t)
             rop = {SUM: dist.ReduceOp.SUM, MAX: dist.ReduceOp.MAX, MIN: dist.ReduceOp.MIN}[op]
             if self.host_staging and t.is_cuda:
                 h = t.cpu()
