@@ -148,3 +148,31 @@ def test_ozaki_nonfinite_rows_and_empty_k(L):
     L.call("skb_gemm_ozaki", 0, 0, M, N, 0, 1.0, _t(A), K, _t(B), N, 0.5, Cd, N, 0, ws, cap,
            stream_ptr())
     assert np.array_equal(Cd.cpu().numpy(), 0.5 * C0)
+
+
+def test_ozaki_thread_pool_matches_sequential(L):
+    """Concurrent host threads (run_comparison's ThreadPoolExecutor pattern)
+    share the cuBLASLt handle: results stay bitwise equal to sequential calls."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2209_08722_b200.runtime import stream_ptr, workspace
+    shapes = [(300, 200, 3000), (128, 512, 2048), (700, 333, 1500), (64, 64, 5000)]
+    data = []
+    for i, (M, N, K) in enumerate(shapes):
+        g = np.random.Generator(np.random.Philox(100 + i))
+        data.append((g.standard_normal((M, K)), g.standard_normal((K, N))))
+
+    def run(i):
+        M, N, K = shapes[i]
+        A, B = data[i]
+        C = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+        ws, cap = workspace(int(L.lib().skb_gemm_ozaki_workspace_bytes(M, N, K)))
+        L.call("skb_gemm_ozaki", 0, 0, M, N, K, 1.0, _t(A), K, _t(B), N, 0.0, C, N, 0, ws, cap,
+               stream_ptr())
+        torch.cuda.current_stream().synchronize()
+        return C.cpu().numpy()
+
+    alone = [run(i) for i in range(len(shapes))]
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        together = list(pool.map(run, range(len(shapes))))
+    for a, b in zip(alone, together):
+        assert np.array_equal(a, b)
