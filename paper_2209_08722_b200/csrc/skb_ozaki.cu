@@ -468,7 +468,7 @@ static int chunk(const skb_oz_args& g, int k0, int Kc, double beta, skb_ws* ws, 
     // k split so the grid covers the GPU ~4x (row blocks alone are too few at m ~ 2e3)
     const int rb = sk == 1 ? (R + 7) / 8 : (R + 31) / 32;
     const int want = std::max(1, (4 * skb_num_sms() + rb - 1) / rb);
-    const int kchunk = std::max(256, (int)up((Kc + want - 1) / want, 256));
+    const int kchunk = std::min(4096, std::max(256, (int)up((Kc + want - 1) / want, 256)));
     dim3 gm(rb, (Kc + kchunk - 1) / kchunk);
     rowmax_kernel<<<gm, 256, 0, st>>>(p0, sr, sk, R, Kc, kk, kchunk, tri, k0, am);
     scales_kernel<<<(Rp + 255) / 256, 256, 0, st>>>(am, R, Rp, mul, inv);
