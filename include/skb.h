@@ -36,8 +36,8 @@ extern "C" {
 #define SKB_ERR_INTERNAL (-5)
 #define SKB_ERR_UNSUPPORTED (-6)
 
-#define SKB_ST_BREAKDOWN_CURV 1  /* errors.Breakdown (krylov_solvers.py:353-354) */
-#define SKB_ST_BREAKDOWN_RZ 2    /* errors.Breakdown (krylov_solvers.py:341-342,360-361) */
+#define SKB_ST_BREAKDOWN_CURV 1  /* errors.Breakdown (krylov_solvers.py:89-90; chebyshev :191-192) */
+#define SKB_ST_BREAKDOWN_RZ 2    /* errors.Breakdown (krylov_solvers.py:77-78,96-97) */
 #define SKB_ST_CHOL_FAIL 4       /* errors.RankDeficient (preconditioning.py:47-50) */
 #define SKB_ST_NONPOSITIVE 8     /* errors.NonpositiveScaling / NonpositivePoint */
 
@@ -240,7 +240,9 @@ int64_t skb_gemm_ozaki_calls(void);
  * m-vector (reference: the single-process sums of krylov_solvers.py:46-47,
  * ipm_core.py:196-242). Peers' symmetric buffers ([2][ld] doubles) and flag
  * words (>= skb_p2p_max_blocks(m) u64) are opened with skb_ipc_open; mode 0 =
- * publish + gather, 1 / 2 = one half (single-process tests). */
+ * publish + gather, 1 / 2 = one half (single-process tests). A peer whose flag
+ * is not seen within timeout_cycles (SM clock) sets *err = 1 (sticky) and the
+ * result is NaN; the caller reads err with its per-step scalars and raises. */
 int skb_p2p_alloc(int64_t bytes, uint64_t* dev_ptr_out);
 int skb_p2p_free(uint64_t dev_ptr);
 int skb_ipc_handle(void* dev_ptr, void* handle_out);
@@ -250,7 +252,8 @@ int32_t skb_p2p_can_access(int32_t device, int32_t peer);
 int32_t skb_p2p_max_blocks(int64_t m);
 int skb_p2p_allreduce(const double* local, double* out, int64_t m, int64_t ld, int32_t rank,
                       int32_t world, const uint64_t* data_ptrs, const uint64_t* flag_ptrs,
-                      uint64_t epoch, int32_t mode, int* err, void* stream);
+                      uint64_t epoch, int32_t mode, int64_t timeout_cycles, int* err,
+                      void* stream);
 
 /* Blocked Cholesky (lower, in place) and triangular inverse; Mp % 64 == 0.
  * status: device int, SKB_ST_CHOL_FAIL on a nonpositive pivot. */

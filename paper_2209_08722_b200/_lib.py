@@ -12,6 +12,8 @@ import ctypes
 import os
 import re
 
+from .errors import DeviceError
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 HEADER = os.path.join(ROOT, "include", "skb.h")
@@ -29,8 +31,9 @@ _CTYPES = {
 }
 
 
-class SkbError(RuntimeError):
-    """A libskb call returned a negative SKB_ERR_* code."""
+class SkbError(DeviceError):
+    """A libskb call returned a negative SKB_ERR_* code (a SkipmError, so the
+    reference CLI's `except SkipmError` maps it to its numeric exit code)."""
 
     NAMES = {-1: "SKB_ERR_ARG", -2: "SKB_ERR_DIMS", -3: "SKB_ERR_WORKSPACE",
              -4: "SKB_ERR_CUDA", -5: "SKB_ERR_INTERNAL", -6: "SKB_ERR_UNSUPPORTED"}

@@ -15,8 +15,8 @@ constexpr int kWarp = 32;
 // them onto the reference exception classes (include/skb.h).
 enum : int {
   ST_OK = 0,
-  ST_BREAKDOWN_CURV = 1,   // krylov_solvers.py:353-354
-  ST_BREAKDOWN_RZ = 2,     // krylov_solvers.py:341-342,360-361
+  ST_BREAKDOWN_CURV = 1,   // krylov_solvers.py:89-90 (chebyshev :191-192)
+  ST_BREAKDOWN_RZ = 2,     // krylov_solvers.py:77-78,96-97
   ST_CHOL_FAIL = 4,        // nonpositive pivot in a Cholesky (rank loss)
   ST_NONPOSITIVE = 8,      // nonpositive scaling / point
   ST_BAD_ARG = 16,

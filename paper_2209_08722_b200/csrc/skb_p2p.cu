@@ -45,7 +45,7 @@ SKB_DEV uint64_t ld_acquire_sys(const uint64_t* p) {
 __global__ void __launch_bounds__(kP2PThreads)
     p2p_allreduce_kernel(const double* __restrict__ local, double* __restrict__ out, int m,
                          int64_t ld, int rank, int world, P2PPeers peers, uint64_t epoch,
-                         int mode, int* err) {
+                         int mode, long long timeout_cycles, int* err) {
   const int b = blockIdx.x;
   const int r0 = b * kP2PThreads, r = r0 + threadIdx.x;
   const int slot = (int)(epoch & 1);
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kP2PThreads)
     const long long t0 = clock64();
     for (int g = 0; g < world; ++g) {
       while (ld_acquire_sys(&peers.flags[g][b]) < epoch) {
-        if (clock64() - t0 > 4000000000ll) {  // ~2 s at 1.9 GHz
+        if (clock64() - t0 > timeout_cycles) {  // default ~2 s at 1.9 GHz
           ok = 0;
           atomicExch(err, 1);
           break;
@@ -146,9 +146,9 @@ extern "C" int32_t skb_p2p_max_blocks(int64_t m) {
 extern "C" int skb_p2p_allreduce(const double* local, double* out, int64_t m, int64_t ld,
                                  int32_t rank, int32_t world, const uint64_t* data_ptrs,
                                  const uint64_t* flag_ptrs, uint64_t epoch, int32_t mode,
-                                 int* err, void* stream) {
+                                 int64_t timeout_cycles, int* err, void* stream) {
   if (world < 1 || world > kP2PMaxRanks || rank < 0 || rank >= world || m < 0 || ld < m ||
-      epoch == 0)
+      epoch == 0 || timeout_cycles <= 0)
     return SKB_ERR_ARG;
   if (m == 0) return 0;
   P2PPeers p{};
@@ -158,6 +158,6 @@ extern "C" int skb_p2p_allreduce(const double* local, double* out, int64_t m, in
   }
   const int grid = (int)((m + kP2PThreads - 1) / kP2PThreads);
   p2p_allreduce_kernel<<<grid, kP2PThreads, 0, (cudaStream_t)stream>>>(
-      local, out, (int)m, ld, rank, world, p, epoch, mode, err);
+      local, out, (int)m, ld, rank, world, p, epoch, mode, (long long)timeout_cycles, err);
   return skb_launch_status(__func__);
 }

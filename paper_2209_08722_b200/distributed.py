@@ -85,11 +85,31 @@ class P2PAllreduce:
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
         from . import _lib
         from .runtime import stream_ptr
+        if t.numel() == 0:  # no launch: the epoch (slot parity) must not move
+            return t
         self.epoch += 1
         _lib.call("skb_p2p_allreduce", t, t, t.numel(), self.ld, self.rank, self.world,
                   self.data_ptrs.ctypes.data, self.flag_ptrs.ctypes.data, self.epoch, 0,
-                  self.err, stream_ptr())
+                  p2p_timeout_cycles(), self.err, stream_ptr())
         return t
+
+    def check(self):
+        """Raise CollectiveTimeout if any exchange so far saw a peer time out
+        (the kernel's sticky err word; one 4-byte read, done with the solve's
+        per-step host scalars)."""
+        if self.err is not None and int(self.err.item()) != 0:
+            from .errors import CollectiveTimeout
+            raise CollectiveTimeout(
+                f"rank {self.rank}: a peer did not join an NVLink all-reduce within "
+                f"{p2p_timeout_cycles()} SM cycles (epoch <= {self.epoch}); the exchanged "
+                "m-vector was poisoned with NaN")
+
+
+def p2p_timeout_cycles() -> int:
+    """Peer-flag wait budget of the NVLink all-reduce in SM cycles:
+    SKB_P2P_TIMEOUT_S seconds (default 2) at the B200's 1.965 GHz boost clock."""
+    import os
+    return max(1, int(float(os.environ.get("SKB_P2P_TIMEOUT_S", "2")) * 1.965e9))
 
 
 def _p2p_enabled_env() -> bool:
@@ -293,6 +313,11 @@ class Comm:
             off = int(all_sizes[h][: self.rank].sum())
             pieces.append(bufs[h][off:off + int(all_sizes[h][self.rank])])
         return torch.cat(pieces).to(t.device)
+
+    def check(self):
+        """Surface an asynchronous exchange failure (CollectiveTimeout)."""
+        if self._p2p is not None:
+            self._p2p.check()
 
     def barrier(self):
         if self.world > 1:

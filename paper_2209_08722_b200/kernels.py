@@ -40,6 +40,16 @@ class DeviceMatrix:
             A = A.toarray()
         A = np.asarray(A, dtype=np.float64)
         m, n = A.shape
+        if A.flags.c_contiguous and 8 * m * n >= (1 << 30):
+            free, _ = torch.cuda.mem_get_info(device)
+            if free > 2.2 * 8 * m * n:  # row-major upload, transpose in HBM
+                rows = torch.empty((m, n), dtype=F64, device=device)
+                step = max(1, (1 << 28) // (8 * n))
+                for i0 in range(0, m, step):
+                    rows[i0:i0 + step].copy_(torch.from_numpy(A[i0:i0 + step]))
+                out = cls.from_rows_device(rows)
+                del rows
+                return out
         cols = torch.zeros((n, lda_for(m)), dtype=F64, device=device)
         step = max(1, (1 << 28) // max(1, 8 * m))  # upload in ~256 MB column slabs
         for j0 in range(0, n, step):

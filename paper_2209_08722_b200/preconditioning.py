@@ -9,11 +9,21 @@ GEMMs, csrc/skb_dense.cu), so
     apply_pinv_adw(f, r) = X (Linv' (Linv r))      = ADW' Q^-1 r = (ADW)^+ r
 
 which equal the reference's operators whenever ADW has full row rank (the
-only case the reference lets through). Rank test: the reference raises
-RankDeficient when sigma_min/sigma_max < 1e-12; since sigma_min(L) <=
-min|L_ii| and sigma_max(L) >= max|L_ii|, a diagonal ratio below the
-tolerance proves deficiency, and a Cholesky breakdown that survives the
-shifted CholeskyQR3 retry is reported the same way.
+only case the reference lets through).
+
+Rank test (rank_check): the reference raises RankDeficient when
+sigma_min/sigma_max of ADW is below 1e-12 (preconditioning.py:47-50). ADW
+and L share their singular values (Q = ADW ADW' = L L'), so the same ratio
+is decided from the factor, two-sided:
+  * upper bounds of the ratio (below the tolerance => deficient): the
+    diagonal ratio min|L_ii| / max|L_ii|, and, when needed, the converged
+    power-iteration estimates of lambda_max(Q) and lambda_max(Q^-1)
+    (Rayleigh quotients approach the extremes from below);
+  * a lower bound (at or above the tolerance => full rank):
+    1 / (||L||_F ||L^-1||_F), with ||L||_F = ||ADW||_F. It is within a factor
+    m of the true ratio, so the power iterations run only in that gray band.
+A Cholesky breakdown that survives the shifted CholeskyQR3 retry is reported
+the same way.
 """
 
 from __future__ import annotations
@@ -77,8 +87,86 @@ def build_preconditioner(X: DeviceMatrix, rank_tol: float = RANK_TOL,
     if int(status) & 4 or not (dmax > 0.0) or not np.isfinite(dmin) or dmin / dmax < rank_tol:
         raise RankDeficient(
             f"ADW numerically rank deficient: diagonal ratio {dmin / max(dmax, 1e-300):.3e}")
-    return PreconditionerFactor(Linv, LinvT, Lfac, X, m, float(dmin), float(dmax), bool(shifted),
-                                sketch_tag)
+    f = PreconditionerFactor(Linv, LinvT, Lfac, X, m, float(dmin), float(dmax), bool(shifted),
+                             sketch_tag)
+    rank_check(f, rank_tol)
+    return f
+
+
+def _adwt(f: PreconditionerFactor, z: torch.Tensor) -> torch.Tensor:
+    """ADW' z for this rank's buckets (w_local-vector)."""
+    u = torch.empty(f.X.n, dtype=F64, device=z.device)
+    if f.X.n > 0:
+        _lib.call("skb_rowdot_gemv", f.X.cols, f.X.lda, f.X.n, f.m, 0, z, u, None, stream_ptr())
+    return u
+
+
+def _q_apply(f: PreconditionerFactor, z: torch.Tensor) -> torch.Tensor:
+    """Q z = ADW (ADW' z), ranks' bucket blocks summed."""
+    u = _adwt(f, z)
+    if f.dist is None:
+        from . import kernels as K
+        out = torch.empty(f.m, dtype=F64, device=z.device)
+        K.gemv(f.X, u, out)
+        return out
+    w_total, r0, comm = f.dist
+    full = torch.zeros(w_total, dtype=F64, device=z.device)
+    full[r0:r0 + f.X.n] = u
+    return reconstruct(f, full)
+
+
+def _lambda_max(apply, m: int, dev, max_iter: int = 300, rtol: float = 1e-9) -> float:
+    """Largest eigenvalue of an SPD operator by power iteration from a fixed
+    start (deterministic); the Rayleigh quotients increase toward it."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(20220918)
+    v = torch.randn(m, dtype=F64, device=dev, generator=g)
+    v /= torch.linalg.vector_norm(v)
+    lam = 0.0
+    for _ in range(max_iter):
+        w = apply(v)
+        new = float(torch.dot(v, w).item())
+        nrm = torch.linalg.vector_norm(w)
+        if not (new > 0.0) or not np.isfinite(new):
+            return new
+        v = w / nrm
+        if abs(new - lam) <= rtol * new:
+            return new
+        lam = new
+    return lam
+
+
+def sigma_ratio_bounds(f: PreconditionerFactor, exact: bool = False):
+    """(lower, upper) bounds of sigma_min/sigma_max of ADW from the factor;
+    exact=True tightens the upper bound with converged power iterations."""
+    m = f.m
+    dev = f.Linv.device
+    x_fro = (torch.linalg.vector_norm(f.X.cols[:, :m]) ** 2).reshape(1) if f.X.n > 0 else \
+        torch.zeros(1, dtype=F64, device=dev)
+    if f.dist is not None:
+        f.dist[2].allreduce_(x_fro)
+    l_fro = torch.linalg.vector_norm(f.Linv[:m, :m]) ** 2
+    fx, fl = (float(v) for v in to_host(torch.cat([x_fro.reshape(1), l_fro.reshape(1)])))
+    lower = 1.0 / np.sqrt(fx * fl) if fx > 0 and fl > 0 else 0.0
+    upper = f.diag_min / f.diag_max if f.diag_max > 0 else 0.0
+    if exact:
+        lq = _lambda_max(lambda v: _q_apply(f, v), m, dev)
+        lqi = _lambda_max(lambda v: apply_inv(f, v), m, dev)
+        if lq > 0 and lqi > 0:
+            upper = min(upper, 1.0 / np.sqrt(lq * lqi))
+    return lower, upper
+
+
+def rank_check(f: PreconditionerFactor, rank_tol: float = RANK_TOL) -> None:
+    """RankDeficient iff sigma_min/sigma_max(ADW) < rank_tol (preconditioning.py:47-50)."""
+    lower, upper = sigma_ratio_bounds(f)
+    if upper < rank_tol:
+        raise RankDeficient(f"ADW numerically rank deficient: sigma ratio <= {upper:.3e}")
+    if lower >= rank_tol:
+        return
+    lower, upper = sigma_ratio_bounds(f, exact=True)
+    if upper < rank_tol:
+        raise RankDeficient(f"ADW numerically rank deficient: sigma ratio ~ {upper:.3e}")
 
 
 def _gemm(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower, ws, cap):
@@ -151,8 +239,10 @@ def _build_distributed(X: DeviceMatrix, rank_tol: float, sketch_tag) -> Precondi
     if not (dmax > 0.0) or not np.isfinite(dmin) or dmin / dmax < rank_tol:
         raise RankDeficient(
             f"ADW numerically rank deficient: diagonal ratio {dmin / max(dmax, 1e-300):.3e}")
-    return PreconditionerFactor(Linv, LinvT, None, X, m, dmin, dmax, shifted, sketch_tag,
-                                dist=X.dist)
+    f = PreconditionerFactor(Linv, LinvT, None, X, m, dmin, dmax, shifted, sketch_tag,
+                             dist=X.dist)
+    rank_check(f, rank_tol)
+    return f
 
 
 def _tri_gemv(M: torch.Tensor, m: int, tri: int, x: torch.Tensor, y: torch.Tensor, gate=None):

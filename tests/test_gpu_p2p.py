@@ -12,6 +12,9 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
+TMO = 4_000_000_000  # peer-flag timeout in SM cycles (~2 s)
+
+
 @pytest.fixture(scope="module")
 def L():
     if not torch.cuda.is_available():
@@ -47,13 +50,13 @@ def test_p2p_allreduce_rank_order(L, world, m):
         for r in range(world):  # everyone else publishes first
             if r != gatherer:
                 L.call("skb_p2p_allreduce", outs[r], outs[r], m, ld, r, world, data.ctypes.data,
-                       flags.ctypes.data, epoch, 1, err, stream_ptr())
+                       flags.ctypes.data, epoch, 1, TMO, err, stream_ptr())
         L.call("skb_p2p_allreduce", outs[gatherer], outs[gatherer], m, ld, gatherer, world,
-               data.ctypes.data, flags.ctypes.data, epoch, 0, err, stream_ptr())
+               data.ctypes.data, flags.ctypes.data, epoch, 0, TMO, err, stream_ptr())
         for r in range(world):
             if r != gatherer:
                 L.call("skb_p2p_allreduce", outs[r], outs[r], m, ld, r, world, data.ctypes.data,
-                       flags.ctypes.data, epoch, 2, err, stream_ptr())
+                       flags.ctypes.data, epoch, 2, TMO, err, stream_ptr())
         for o in outs:
             assert np.array_equal(o.cpu().numpy(), ref)
     assert int(err.item()) == 0
@@ -68,8 +71,9 @@ def test_p2p_allreduce_times_out_instead_of_hanging(L):
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     x = torch.ones(m, dtype=torch.float64, device="cuda")
     # rank 0 gathers epoch 1 but rank 1 never publishes it
+    # a short, configurable timeout (0.05 s of SM clock)
     L.call("skb_p2p_allreduce", x, x, m, ld, 0, world, data.ctypes.data, flags.ctypes.data, 1, 0,
-           err, stream_ptr())
+           100_000_000, err, stream_ptr())
     torch.cuda.synchronize()
     assert int(err.item()) == 1 and torch.isnan(x).all()
     for p in list(data) + list(flags):
