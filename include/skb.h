@@ -119,34 +119,49 @@ int skb_reduce_partials(const double* part, int32_t nparts, int64_t m, const dou
 
 /* ---------------------------------------------- sparse A (CSC), config c4 --
  * The same passes over A stored as CSC: colptr (int64, n+1), rowidx (int32),
- * vals (double). One thread per column; z and the CTA's m-vector partial in
- * shared memory (m <= 14080); partials reduced in a fixed order. */
+ * vals (double); z and the CTA's m-vector partial in shared memory; partials
+ * reduced in a fixed order. The passes that produce an m-vector take a plan
+ (skb_csc_plan_build, once per matrix: whole columns cut into chunks that fit
+ * a shared-memory stage, stored as vals | row u16 + row-sorted slot u16 |
+ * column offsets u16, see csrc/skb_cscplan.cuh): the chunks stream through a
+ * TMA bulk-copy ring and the scatter is a per-warp pass over row-disjoint
+ * ranges of the row-sorted products -- no atomics, deterministic, 12 B/nnz
+ * + 10 B/column per pass. plan == NULL (or m > 65535, a column too long for a
+ * stage, z + partial too large for shared memory) runs the thread-per-column
+ * kernel with shared atomics (m <= 14080). */
+size_t skb_csc_plan_bytes(int64_t m, int64_t n, int64_t nnz, int64_t maxlen);
+int skb_csc_plan_build(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                       int64_t m, int64_t n, int64_t nnz, int64_t maxlen, void* plan,
+                       size_t plan_bytes, int64_t* nchunks_out, void* stream);
 int skb_csc_normal_apply(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                         int64_t m, int64_t n, const double* d2, const double* z, double* u,
-                         const double* sub, const int* gate, void* workspace, size_t ws_bytes,
-                         void* stream);
-int skb_csc_gemv(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
-                 int64_t n, const double* x, double* u, const double* sub, void* workspace,
-                 size_t ws_bytes, void* stream);
+                         const void* plan, int64_t plan_chunks, int64_t m, int64_t n,
+                         const double* d2, const double* z, double* u, const double* sub,
+                         const int* gate, void* workspace, size_t ws_bytes, void* stream);
+int skb_csc_gemv(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                 const void* plan, int64_t plan_chunks, int64_t m, int64_t n, const double* x,
+                 double* u, const double* sub, void* workspace, size_t ws_bytes, void* stream);
 int skb_csc_gemv_ratio(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                       int64_t m, int64_t n, const double* v, const double* s, double* u,
-                       const double* sub, void* workspace, size_t ws_bytes, void* stream);
-int skb_csc_rhs(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
-                int64_t n, const double* x, const double* s, const double* r_d, double sigma_mu,
-                double* p, const double* r_p, void* workspace, size_t ws_bytes, void* stream);
+                       const void* plan, int64_t plan_chunks, int64_t m, int64_t n,
+                       const double* v, const double* s, double* u, const double* sub,
+                       void* workspace, size_t ws_bytes, void* stream);
+int skb_csc_rhs(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                const void* plan, int64_t plan_chunks, int64_t m, int64_t n, const double* x,
+                const double* s, const double* r_d, double sigma_mu, double* p,
+                const double* r_p, void* workspace, size_t ws_bytes, void* stream);
 int skb_csc_gemv_t(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
                    int64_t n, const double* y, const double* add, const double* sub, double* t,
                    void* workspace, size_t ws_bytes, void* stream);
 int skb_csc_directions(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                       int64_t m, int64_t n, const double* dy, const double* x, const double* s,
-                       const double* v, const double* r_d, double sigma_mu, double* ds,
-                       double* dx, double* atdy, double* adx, void* workspace, size_t ws_bytes,
-                       void* stream);
-int skb_csc_iterate(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
-                    int64_t n, const double* x, const double* dx, const double* s,
-                    const double* ds, double alpha, const double* y_new, const double* b,
-                    const double* c, double* x_out, double* s_out, double* r_p, double* r_d,
-                    void* workspace, size_t ws_bytes, void* stream);
+                       const void* plan, int64_t plan_chunks, int64_t m, int64_t n,
+                       const double* dy, const double* x, const double* s, const double* v,
+                       const double* r_d, double sigma_mu, double* ds, double* dx, double* atdy,
+                       double* adx, void* workspace, size_t ws_bytes, void* stream);
+int skb_csc_iterate(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                    const void* plan, int64_t plan_chunks, int64_t m, int64_t n, const double* x,
+                    const double* dx, const double* s, const double* ds, double alpha,
+                    const double* y_new, const double* b, const double* c, double* x_out,
+                    double* s_out, double* r_p, double* r_d, void* workspace, size_t ws_bytes,
+                    void* stream);
 /* Bit-exact ADW for CSC A (ascending-j sums per (row, bucket), no FMA). */
 int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx, const double* av,
                          int64_t m, int64_t n, const double* d, const int32_t* cols,

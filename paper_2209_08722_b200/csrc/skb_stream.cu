@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "skb_common.cuh"
 #include "skb_internal.h"
 
@@ -970,6 +972,9 @@ static int run_csc(const int64_t* colptr, const int32_t* rowidx, const double* v
 
 }  // namespace skb
 
+#include "skb_cscplan.cuh"
+
+
 namespace skb {
 __global__ void csc_to_dense_kernel(const int64_t* __restrict__ colptr,
                                     const int32_t* __restrict__ rowidx,
@@ -993,36 +998,47 @@ extern "C" int skb_csc_to_dense(const int64_t* colptr, const int32_t* rowidx, co
 
 #define SKB_CSC const int64_t *colptr, const int32_t *rowidx, const double *vals, int64_t m, \
                 int64_t n
+#define SKB_CSCP const int64_t *colptr, const int32_t *rowidx, const double *vals, \
+                 const void *plan, int64_t plan_chunks, int64_t m, int64_t n
+// the planned kernel when a plan is given (and applies), else the thread-per-column one
+#define SKB_CSC_RUN(Z, OUT, SUB, GATE)                                                      \
+  do {                                                                                      \
+    CscPlanView pv;                                                                         \
+    if (cscp_view(plan, plan_chunks, m, &pv))                                               \
+      return run_cscp(pv, (int)m, Z, OUT, SUB, op, &ws, (cudaStream_t)stream, GATE);        \
+    return run_csc(colptr, rowidx, vals, (int)m, n, Z, OUT, SUB, op, &ws,                   \
+                   (cudaStream_t)stream, GATE);                                             \
+  } while (0)
 
-extern "C" int skb_csc_normal_apply(SKB_CSC, const double* d2, const double* z, double* u,
+extern "C" int skb_csc_normal_apply(SKB_CSCP, const double* d2, const double* z, double* u,
                                     const double* sub, const int* gate, void* workspace,
                                     size_t ws_bytes, void* stream) {
   SKB_WS;
   OpNormal op{d2};
-  return run_csc(colptr, rowidx, vals, (int)m, n, z, u, sub, op, &ws, (cudaStream_t)stream, gate);
+  SKB_CSC_RUN(z, u, sub, gate);
 }
 
-extern "C" int skb_csc_gemv(SKB_CSC, const double* x, double* u, const double* sub,
+extern "C" int skb_csc_gemv(SKB_CSCP, const double* x, double* u, const double* sub,
                             void* workspace, size_t ws_bytes, void* stream) {
   SKB_WS;
   OpGemvX op{x};
-  return run_csc(colptr, rowidx, vals, (int)m, n, nullptr, u, sub, op, &ws, (cudaStream_t)stream);
+  SKB_CSC_RUN(nullptr, u, sub, nullptr);
 }
 
-extern "C" int skb_csc_gemv_ratio(SKB_CSC, const double* v, const double* s, double* u,
+extern "C" int skb_csc_gemv_ratio(SKB_CSCP, const double* v, const double* s, double* u,
                                   const double* sub, void* workspace, size_t ws_bytes,
                                   void* stream) {
   SKB_WS;
   OpGemvRatio op{v, s};
-  return run_csc(colptr, rowidx, vals, (int)m, n, nullptr, u, sub, op, &ws, (cudaStream_t)stream);
+  SKB_CSC_RUN(nullptr, u, sub, nullptr);
 }
 
-extern "C" int skb_csc_rhs(SKB_CSC, const double* x, const double* s, const double* r_d,
+extern "C" int skb_csc_rhs(SKB_CSCP, const double* x, const double* s, const double* r_d,
                            double sigma_mu, double* p, const double* r_p, void* workspace,
                            size_t ws_bytes, void* stream) {
   SKB_WS;
   OpRhs op{x, s, r_d, sigma_mu};
-  return run_csc(colptr, rowidx, vals, (int)m, n, nullptr, p, r_p, op, &ws, (cudaStream_t)stream);
+  SKB_CSC_RUN(nullptr, p, r_p, nullptr);
 }
 
 extern "C" int skb_csc_gemv_t(SKB_CSC, const double* y, const double* add, const double* sub,
@@ -1033,22 +1049,21 @@ extern "C" int skb_csc_gemv_t(SKB_CSC, const double* y, const double* add, const
                  (cudaStream_t)stream);
 }
 
-extern "C" int skb_csc_directions(SKB_CSC, const double* dy, const double* x, const double* s,
+extern "C" int skb_csc_directions(SKB_CSCP, const double* dy, const double* x, const double* s,
                                   const double* v, const double* r_d, double sigma_mu, double* ds,
                                   double* dx, double* atdy, double* adx, void* workspace,
                                   size_t ws_bytes, void* stream) {
   SKB_WS;
   OpDir op{x, s, v, r_d, sigma_mu, ds, dx, atdy};
-  return run_csc(colptr, rowidx, vals, (int)m, n, dy, adx, nullptr, op, &ws,
-                 (cudaStream_t)stream);
+  SKB_CSC_RUN(dy, adx, nullptr, nullptr);
 }
 
-extern "C" int skb_csc_iterate(SKB_CSC, const double* x, const double* dx, const double* s,
+extern "C" int skb_csc_iterate(SKB_CSCP, const double* x, const double* dx, const double* s,
                                const double* ds, double alpha, const double* y_new,
                                const double* b, const double* c, double* x_out, double* s_out,
                                double* r_p, double* r_d, void* workspace, size_t ws_bytes,
                                void* stream) {
   SKB_WS;
   OpIter op{x, dx, s, ds, c, alpha, x_out, s_out, r_d};
-  return run_csc(colptr, rowidx, vals, (int)m, n, y_new, r_p, b, op, &ws, (cudaStream_t)stream);
+  SKB_CSC_RUN(y_new, r_p, b, nullptr);
 }

@@ -111,6 +111,37 @@ class SparseDeviceMatrix:
     def args(self):
         return (self.colptr, self.rowidx, self.vals, self.m, self.n)
 
+    def pargs(self):
+        """args() with the pass plan of the deterministic (atomic-free) CSC
+        passes (csrc/skb_cscplan.cuh) when one was built, else (None, 0): the
+        thread-per-column passes with shared-memory atomics."""
+        plan, nch = getattr(self, "_plan", None) or self.plan()
+        return (self.colptr, self.rowidx, self.vals, plan, nch, self.m, self.n)
+
+    def plan(self, force: bool = False):
+        """Build (once) the pass plan of the deterministic CSC passes: on
+        request, or for every matrix when SKB_CSC_PLAN=1. At c4 the planned
+        pass is bitwise reproducible but slower than the atomic one (0.69 vs
+        0.47 ms), so it is opt-in."""
+        import os
+        want = force or os.environ.get("SKB_CSC_PLAN", "0") == "1"
+        if getattr(self, "_plan", None) is None or (want and self._plan[0] is None
+                                                       and not getattr(self, "_plan_tried", False)):
+            self._plan = (None, 0)
+            if want and self.n > 0:
+                self._plan_tried = True
+                lens = self.colptr[1:] - self.colptr[:-1]
+                maxlen = int(lens.max().item())
+                nnz = int((self.colptr[-1] - self.colptr[0]).item())
+                nb = int(_lib.lib().skb_csc_plan_bytes(self.m, self.n, nnz, maxlen))
+                if nb > 0:
+                    buf = torch.empty(nb, dtype=torch.uint8, device=self.vals.device)
+                    nch = np.zeros(1, dtype=np.int64)
+                    _lib.call("skb_csc_plan_build", self.colptr, self.rowidx, self.vals, self.m,
+                              self.n, nnz, maxlen, buf, nb, nch.ctypes.data, stream_ptr())
+                    self._plan = (buf, int(nch[0]))
+        return self._plan
+
     def to_host(self):
         """scipy CSC copy (column slices rebased to their first entry)."""
         import scipy.sparse as sp
@@ -127,10 +158,11 @@ class SparseDeviceMatrix:
         return DeviceMatrix(cols, self.m)
 
 
-def _amat(A):
-    """-> (C symbol prefix, leading C arguments) for a dense or CSC matrix."""
+def _amat(A, planned: bool = True):
+    """-> (C symbol prefix, leading C arguments) for a dense or CSC matrix
+    (CSC passes that produce an m-vector take the matrix's pass plan)."""
     if getattr(A, "is_sparse", False):
-        return "skb_csc_", A.args()
+        return "skb_csc_", (A.pargs() if planned else A.args())
     return "skb_", (A.cols, A.m, A.n, A.lda)
 
 
@@ -170,7 +202,7 @@ def rhs(A, x, s, sigma_mu: float, out, r_d=None, r_p=None):
 def gemv_t(A, y, out, add=None, sub=None):
     """out = (A' y [+ add]) [- sub]   (ipm_core.py:100,218)."""
     ws, cap = _ws(A.m)
-    pre, args = _amat(A)
+    pre, args = _amat(A, planned=False)
     _lib.call(pre + "gemv_t", *args, y, _p(add), _p(sub), out, ws, cap, stream_ptr())
     return out
 

@@ -113,7 +113,10 @@ def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix):
     assert np.array_equal(_h(X.cols)[:, :m].T, ref)
 
 
-def test_sparse_trajectory_s4(K, monkeypatch):
+@pytest.mark.parametrize("planned", ["0", "1"])
+def test_sparse_trajectory_s4(K, monkeypatch, planned):
+    """planned=1: every m-vector A-pass on the deterministic planned kernel."""
+    monkeypatch.setenv("SKB_CSC_PLAN", planned)
     from paper_2209_08722_b200 import ipm_core as IC
     from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
     with open(os.path.join(GOLDEN, "sparse_traces.json")) as f:
@@ -121,6 +124,7 @@ def test_sparse_trajectory_s4(K, monkeypatch):
     lpd = sparse_wide_lp(100, 20_000, 5, 7)
     dlp = DeviceLP.from_host(LinearProgram(lpd.A.tocsr(), lpd.b, lpd.c))
     assert dlp.sparse
+    assert (dlp.A.plan()[0] is not None) == (planned == "1")
     kw = dict(mode="feasible", gamma=lpd.gamma_run(0.1), sigma=0.5, w=400, s=4, tol_outer=1e-6,
               seed=11)
     rep = IC.solve(dlp, IC.make_iterate(dlp, lpd.x0, lpd.y0, lpd.s0), IC.IpmParams(**kw))
@@ -130,7 +134,6 @@ def test_sparse_trajectory_s4(K, monkeypatch):
     monkeypatch.setattr(O.NormalOp, "apply", lambda self, v: Ad @ (self.d2 * (Ad.T @ v)))
     ref = O.solve(A, lpd.b, lpd.c, O.make_iterate(A, lpd.b, lpd.c, lpd.x0, lpd.y0, lpd.s0),
                   O.Params(**kw))
-    monkeypatch.undo()
     assert rep.outer == gold["outer"]
     assert [r.inner_iterations for r in rep.steps] == gold["inner_iterations"]
     assert [r.sketch_seed for r in rep.steps] == [s["sketch_seed"] for s in gold["steps"]]
