@@ -250,6 +250,18 @@ int skb_gemm_ozaki(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, doub
 size_t skb_gemm_ozaki_workspace_bytes(int32_t M, int32_t N, int32_t K);
 int64_t skb_gemm_ozaki_calls(void);
 
+/* Batched INT8 x INT8 -> INT32 GEMM on the tcgen05 tensor cores (TMA-fed,
+ * TMEM accumulators; csrc/skb_i8gemm.cu), the core of the FP64 emulation:
+ * C_l[r][c] = sum_{k in [k0,k1)} A_l[ar0+r][k] B_l[br0+c][k] for l < n, with
+ * K-major int8 slabs (Kp bytes per row, Ra / Rb rows, batch strides sa / sb),
+ * int32 C (row stride ldc, batch stride sc). k0 % 128 == 0, cols % 16 == 0;
+ * entries of [k0, k1) the caller does not want must be zero in the slabs.
+ * tri = 1 computes only the 256 x 256 tiles meeting col <= row + tri_off. */
+int skb_i8gemm_batched(const int8_t* A, int64_t Ra, int64_t sa, const int8_t* B, int64_t Rb,
+                       int64_t sb, int64_t Kp, int32_t* C, int64_t ldc, int64_t sc, int32_t rows,
+                       int32_t cols, int32_t ar0, int32_t br0, int32_t k0, int32_t k1, int32_t n,
+                       int32_t tri, int32_t tri_off, void* stream);
+
 /* One-shot all-reduce of an m-vector over NVLink peer memory (csrc/skb_p2p.cu):
  * the exchange SURVEY.md §8(e) puts after every sharded A-pass that yields an
  * m-vector (reference: the single-process sums of krylov_solvers.py:46-47,

@@ -113,3 +113,5 @@ struct skb_readback {
     return e;
   }
 };
+
+// Batched INT8 GEMM on tcgen05 (skb_i8gemm.cu); declared in include/skb.h.

@@ -12,7 +12,8 @@
 //      precision with respect to the row maximum);
 //   2. reduce a' modulo n small pairwise-coprime moduli p_l <= 256 (symmetric
 //      residues fit int8) — n = 16 covers 2 * 53 + log2 K + 2 bits;
-//   3. n exact INT8 x INT8 -> INT32 GEMMs (cuBLASLt, one strided batch);
+//   3. n exact INT8 x INT8 -> INT32 GEMMs (one batched launch of the
+//      hand-written tcgen05 kernel, skb_i8gemm.cu);
 //   4. per output element, residues of the exact integer product C' and the
 //      Chinese remainder theorem in split-double arithmetic give C' to fp64
 //      accuracy; C = alpha 2^-(sigma_i + tau_j) C' + beta C.
@@ -350,6 +351,13 @@ static Lt& lt() {
 
 constexpr size_t kLtWs = 32u << 20;
 
+// The INT8 products run on the hand-written tcgen05 kernel; SKB_OZ_CUBLASLT=1
+// routes them to cuBLASLt instead (A/B comparisons in development and tests).
+static bool use_cublaslt() {
+  const char* e = getenv("SKB_OZ_CUBLASLT");
+  return e && e[0] == '1';
+}
+
 // c32[l] (rows x cols, row stride ldc) = a8[l] (rows x Kk) * b8[l] (cols x Kk)'
 // for l < n; a8/b8 row stride ld, modulus strides sa / sb, c32 stride sc.
 static int int8_gemm_batched(const int8_t* a8, int64_t sa, const int8_t* b8, int64_t sb,
@@ -421,7 +429,10 @@ static int chunk(const skb_oz_args& g, int k0, int Kc, double beta, skb_ws* ws, 
                      g.M == g.N && g.tri_a == 0 && g.tri_b == 0;
   const bool rslab = g.lower_only || g.tri_a, cslab = g.tri_b != 0;
   int wc = cslab && g.N > 2 * kSlab ? kSlab : Np;
-  int h = rslab && g.M > 2 * kSlab ? kSlab : Mp;
+  // the tcgen05 kernel skips tiles above the diagonal itself: lower_only needs no
+  // row slabs (only triangular operands, whose K ranges shrink per slab, do)
+  const bool tile_tri = g.lower_only && !g.tri_a && !use_cublaslt();
+  int h = rslab && !tile_tri && g.M > 2 * kSlab ? kSlab : Mp;
   const size_t mark = ws->off;
   auto* amA = (unsigned long long*)skb_ws_take(ws, (size_t)Mp * 8);
   auto* amB = share ? amA : (unsigned long long*)skb_ws_take(ws, (size_t)Np * 8);
@@ -440,7 +451,7 @@ static int chunk(const skb_oz_args& g, int k0, int Kc, double beta, skb_ws* ws, 
   const size_t left = ws->cap > ws->off + 1024 ? ws->cap - ws->off - 1024 : 0;
   const size_t per_elem = (size_t)n * 4;
   if ((size_t)h * up(wc, kPadR) * per_elem > left) {
-    h = (int)std::min<int64_t>(h, (int64_t)(left / (per_elem * up(wc, kPadR))) / 128 * 128);
+    h = (int)std::min<int64_t>(h, (int64_t)(left / (per_elem * up(wc, kPadR))) / 256 * 256);
     if (h < 128) {
       h = std::min(Mp, 128);
       wc = (int)std::min<int64_t>(wc, (int64_t)(left / (per_elem * h)) / 256 * 256);
@@ -498,9 +509,18 @@ static int chunk(const skb_oz_args& g, int k0, int Kc, double beta, skb_ws* ws, 
       const int rows = r1 - r0, cols = c1 - c0;
       const int rows_p = (int)up(rows, kPadR), cols_p = (int)up(cols, kPadR);
       if (ke > kb) {
-        rc = int8_gemm_batched(a8 + (int64_t)r0 * Kp + kb, (int64_t)Mp * Kp,
-                               b8 + (int64_t)c0 * Kp + kb, (int64_t)Np * Kp, c32, ldt, mstr,
-                               rows_p, cols_p, ke - kb, Kp, n, lws, st);
+        if (use_cublaslt()) {  // development A/B only (SKB_OZ_CUBLASLT=1)
+          rc = int8_gemm_batched(a8 + (int64_t)r0 * Kp + kb, (int64_t)Mp * Kp,
+                                 b8 + (int64_t)c0 * Kp + kb, (int64_t)Np * Kp, c32, ldt, mstr,
+                                 rows_p, cols_p, ke - kb, Kp, n, lws, st);
+          if (rc == 1) rc = SKB_ERR_UNSUPPORTED;  // never fall back after tiles were written
+        } else {
+          // the tcgen05 kernel (skb_i8gemm.cu); its K range starts on a 128-byte box:
+          // entries in [kb128, kb) of these rows are outside the operand's triangle, zero
+          rc = skb_i8gemm_batched(a8, Mp, (int64_t)Mp * Kp, b8, Np, (int64_t)Np * Kp, Kp, c32,
+                                  ldt, mstr, rows_p, cols_p, r0, c0, kb / 128 * 128, ke, n,
+                                  g.lower_only ? 1 : 0, r0 - c0, st);
+        }
       } else {
         cudaMemsetAsync(c32, 0, (size_t)mstr * per_elem, st);
       }
@@ -551,7 +571,7 @@ int skb_oz_gemm(const skb_oz_args& g, skb_ws* ws, cudaStream_t st) {
                                                                  g.lower_only, g.beta);
     return skb_launch_status("ozaki k=0");
   }
-  if (!oz::lt().ok) return 1;
+  if (oz::use_cublaslt() && !oz::lt().ok) return 1;
   // K chunk: <= kMaxK (exact INT32 sums) and small enough that both residue
   // sets plus a 1024-row INT32 slab fit the workspace; chunks accumulate in fp64.
   const size_t avail = ws->cap > ws->off + 8192 ? ws->cap - ws->off - 8192 : 0;
