@@ -12,7 +12,18 @@ With world_size 1 every method is a no-op.
 
 from __future__ import annotations
 
+import os
+
 import torch
+
+# Reproducible sharded parity: NCCL's sums are identical run to
+# run only for a fixed rank count, message size and algorithm / protocol, so
+# unless the user chose them (or SKB_NCCL_PIN=0) they are pinned here, before
+# any communicator exists (import this package before init_process_group). The
+# per-pass m-vector exchange does not go through NCCL at all (P2PAllreduce).
+if os.environ.get("SKB_NCCL_PIN", "1") != "0":
+    for _k, _v in (("NCCL_ALGO", "Ring"), ("NCCL_PROTO", "Simple")):
+        os.environ.setdefault(_k, _v)
 
 try:
     import torch.distributed as dist

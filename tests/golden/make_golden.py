@@ -37,7 +37,9 @@ HASH_CASES = [
     (1, 1, 1, 22),
 ]
 BIG_HASH_CASES = [(1_000_000, 4_000, 1, 31), (1_000_000, 4_000, 4, 32),
-                  (4_000_000, 8_000, 1, 33)]
+                  (4_000_000, 8_000, 1, 33),
+                  (20_000_000, 40_000, 4, 34),  # config c4 at s = 4 (the parity setting)
+                  (4_000_000, 8_000, 4, 35)]    # config c3 at s = 4
 
 
 def sha(a: np.ndarray) -> str:

@@ -80,3 +80,21 @@ def test_sharded_host_logic_world2():
     assert res[0][4] == (0, 502) and res[1][4] == (502, 1003)
     for _, err, ok_stats, ok_gather, _, ok_dist in res:
         assert err <= 1e-13 and ok_stats and ok_gather and ok_dist
+
+
+def test_nccl_algorithm_pinned_for_reproducible_sums():
+    """NCCL_ALGO / NCCL_PROTO pinned on import unless set."""
+    import os
+    import subprocess
+    import sys
+    code = ("import os; import paper_2209_08722_b200.distributed; "
+            "print(os.environ['NCCL_ALGO'], os.environ['NCCL_PROTO'])")
+    env = {k: v for k, v in os.environ.items() if k not in ("NCCL_ALGO", "NCCL_PROTO")}
+    root = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+    out = subprocess.run([sys.executable, "-c", code], env=dict(env, PYTHONPATH=root),
+                         capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.stdout.split() == ["Ring", "Simple"], out.stderr
+    out = subprocess.run([sys.executable, "-c", code],
+                         env=dict(env, PYTHONPATH=root, NCCL_ALGO="Tree"),
+                         capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.stdout.split() == ["Tree", "Simple"], out.stderr

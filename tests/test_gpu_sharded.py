@@ -100,7 +100,10 @@ def test_sharded_solve_matches_reference(world, kind):
         assert seeds == [s["sketch_seed"] for s in gold["steps"]]
         assert nx == n_lp
         dev = np.abs(np.array(mu) - np.array(gold["mu_trace"])) / np.array(gold["mu_trace"])
-        # sharded sums change the summation order: same floor as a reordered reference
+        # sharded sums change the summation order: the small LP's late steps amplify
+        # any reordering of the reference itself to ~1.1e-8
+        print(f"[{kind} rank {rank}] max mu rel dev {dev.max():.2e}, "
+              f"objective rel dev {abs(obj - gold['objective']) / abs(gold['objective']):.2e}")
         assert dev.max() <= 5e-8, dev.max()
         assert abs(obj - gold["objective"]) <= 1e-8 * abs(gold["objective"])
     assert all(r[3] == res[0][3] for r in res)  # replicated scalars identical on every rank
