@@ -130,41 +130,51 @@ int skb_reduce_partials(const double* part, int32_t nparts, int64_t m, const dou
  * stage, z + partial too large for shared memory) runs the thread-per-column
  * kernel with shared atomics (m <= 14080). */
 size_t skb_csc_plan_bytes(int64_t m, int64_t n, int64_t nnz, int64_t maxlen);
+/* ELL head records (m <= 65535): one 64-byte record per column with its first
+ * 5 rows (u16) and values; with them every pass (`ell`, nullable) reads a
+ * column as one contiguous load instead of colptr -> rowidx -> vals. */
+size_t skb_csc_ell_bytes(int64_t m, int64_t n);
+int skb_csc_ell_build(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                      int64_t m, int64_t n, void* ell, size_t ell_bytes, void* stream);
 int skb_csc_plan_build(const int64_t* colptr, const int32_t* rowidx, const double* vals,
                        int64_t m, int64_t n, int64_t nnz, int64_t maxlen, void* plan,
                        size_t plan_bytes, int64_t* nchunks_out, void* stream);
 int skb_csc_normal_apply(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                         const void* plan, int64_t plan_chunks, int64_t m, int64_t n,
+                         const void* plan, int64_t plan_chunks, const void* ell, int64_t m, int64_t n,
                          const double* d2, const double* z, double* u, const double* sub,
                          const int* gate, void* workspace, size_t ws_bytes, void* stream);
 int skb_csc_gemv(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                 const void* plan, int64_t plan_chunks, int64_t m, int64_t n, const double* x,
+                 const void* plan, int64_t plan_chunks, const void* ell, int64_t m, int64_t n, const double* x,
                  double* u, const double* sub, void* workspace, size_t ws_bytes, void* stream);
 int skb_csc_gemv_ratio(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                       const void* plan, int64_t plan_chunks, int64_t m, int64_t n,
+                       const void* plan, int64_t plan_chunks, const void* ell, int64_t m, int64_t n,
                        const double* v, const double* s, double* u, const double* sub,
                        void* workspace, size_t ws_bytes, void* stream);
 int skb_csc_rhs(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                const void* plan, int64_t plan_chunks, int64_t m, int64_t n, const double* x,
+                const void* plan, int64_t plan_chunks, const void* ell, int64_t m, int64_t n, const double* x,
                 const double* s, const double* r_d, double sigma_mu, double* p,
                 const double* r_p, void* workspace, size_t ws_bytes, void* stream);
-int skb_csc_gemv_t(const int64_t* colptr, const int32_t* rowidx, const double* vals, int64_t m,
-                   int64_t n, const double* y, const double* add, const double* sub, double* t,
+int skb_csc_gemv_t(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                   const void* plan, int64_t plan_chunks, const void* ell, int64_t m, int64_t n,
+                   const double* y, const double* add, const double* sub, double* t,
                    void* workspace, size_t ws_bytes, void* stream);
 int skb_csc_directions(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                       const void* plan, int64_t plan_chunks, int64_t m, int64_t n,
+                       const void* plan, int64_t plan_chunks, const void* ell, int64_t m, int64_t n,
                        const double* dy, const double* x, const double* s, const double* v,
                        const double* r_d, double sigma_mu, double* ds, double* dx, double* atdy,
                        double* adx, void* workspace, size_t ws_bytes, void* stream);
 int skb_csc_iterate(const int64_t* colptr, const int32_t* rowidx, const double* vals,
-                    const void* plan, int64_t plan_chunks, int64_t m, int64_t n, const double* x,
+                    const void* plan, int64_t plan_chunks, const void* ell, int64_t m, int64_t n, const double* x,
                     const double* dx, const double* s, const double* ds, double alpha,
                     const double* y_new, const double* b, const double* c, double* x_out,
                     double* s_out, double* r_p, double* r_d, void* workspace, size_t ws_bytes,
                     void* stream);
-/* Bit-exact ADW for CSC A (ascending-j sums per (row, bucket), no FMA). */
+/* Bit-exact ADW for CSC A (ascending-j sums per (row, bucket), no FMA). With
+ * the matrix's ELL records (`ell`, nullable; this call writes d into them) and
+ * 2048 < m <= 65535: one CTA per bucket, records prefetched a batch ahead,
+ * each batch's terms radix-sorted by (row, member) and applied run by run. */
 int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx, const double* av,
-                         int64_t m, int64_t n, const double* d, const int32_t* cols,
+                         void* ell, int64_t m, int64_t n, const double* d, const int32_t* cols,
                          const double* vals, int32_t s, int32_t w, double* X, int64_t ldx,
                          void* workspace, size_t ws_bytes, void* stream);
 /* Dense column-major copy (A zeroed by the caller). */

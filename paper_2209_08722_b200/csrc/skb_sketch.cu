@@ -16,8 +16,10 @@
 //     __dmul_rn/__dadd_rn (no FMA). Splitting rows (not members) across
 //     threads keeps the per-(i, b) summation order of the reference exactly.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_histogram.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
@@ -57,10 +59,17 @@ __global__ void bucket_chunk_prefix_kernel(int32_t* __restrict__ hist, int nchun
 // shared-memory cursor per bucket and writes the entry index to its slot.
 constexpr int kScatterSub = 4096;
 
+// Member codes: the entry index (< 2^31) with the sign of its hash value in bit
+// 31, so a bucket's consumers learn v = +-1/sqrt(s) without gathering vals.
+SKB_DEV uint32_t sign_bit(const double* __restrict__ vals, int64_t e) {
+  return vals[e] < 0.0 ? 0x80000000u : 0u;
+}
+constexpr uint32_t kMemIdx = 0x7FFFFFFFu;
+
 __global__ void __launch_bounds__(256) bucket_scatter_kernel(
     const int32_t* __restrict__ cols, int64_t N, int64_t C, int w,
     const int32_t* __restrict__ hist, const uint64_t* __restrict__ start,
-    int32_t* __restrict__ mem_e) {
+    const double* __restrict__ vals, int32_t* __restrict__ mem_e) {
   extern __shared__ uint32_t sm_scatter[];
   uint32_t* cursor = sm_scatter;
   int32_t* sb = reinterpret_cast<int32_t*>(sm_scatter + w);
@@ -82,7 +91,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
         const int b = sb[t];
         const unsigned peers = __match_any_sync(amask, b);
         const int rank = __popc(peers & ((1u << lane) - 1u));
-        mem_e[cursor[b] + rank] = (int32_t)(s0 + t);
+        mem_e[cursor[b] + rank] = (int32_t)((uint32_t)(s0 + t) | sign_bit(vals, s0 + t));
         __syncwarp(amask);
         if (rank == 0) cursor[b] += __popc(peers);
         __syncwarp(amask);
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(kConsumers + 32, KP <= 4 ? 2 : 1)
         int64_t j = 0;
         double v = 0.0, dj = 0.0;
         if (e < e1) {
-          const int64_t ei = mem_e[e];
+          const int64_t ei = (uint32_t)mem_e[e] & kMemIdx;
           j = ei / s;
           v = vals[ei];
           dj = d[j];
@@ -286,9 +295,9 @@ __global__ void sketch_gather_kernel(const int32_t* __restrict__ cols,
 using namespace skb;
 
 namespace skb {
-__global__ void iota_kernel(int32_t* __restrict__ v, int64_t N) {
+__global__ void iota_kernel(int32_t* __restrict__ v, const double* __restrict__ vals, int64_t N) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < N) v[i] = (int32_t)i;
+  if (i < N) v[i] = (int32_t)((uint32_t)i | sign_bit(vals, i));
 }
 }  // namespace skb
 
@@ -318,7 +327,8 @@ extern "C" size_t skb_sketch_workspace_bytes(int64_t n, int32_t w, int32_t s) {
   return std::max(counting, radix);
 }
 
-static int bucket_sort_radix(const int32_t* cols, int64_t N, int32_t w, skb_ws* ws,
+static int bucket_sort_radix(const int32_t* cols, const double* vals, int64_t N, int32_t w,
+                             skb_ws* ws,
                              cudaStream_t st, uint64_t** start_out, int32_t** mem_out,
                              unsigned int** counter_out) {
   uint32_t* total = (uint32_t*)skb_ws_take(ws, (size_t)w * 4);
@@ -336,7 +346,7 @@ static int bucket_sort_radix(const int32_t* cols, int64_t N, int32_t w, skb_ws* 
   size_t b1 = tb;
   cub::DeviceHistogram::HistogramEven(tmp, b1, cols, total, (int)w + 1, 0, (int)w, (int)N, st);
   scan_buckets_kernel<<<1, 1024, 0, st>>>(total, start, w);
-  iota_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(iota, N);
+  iota_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(iota, vals, N);
   size_t b2 = tb;
   cub::DeviceRadixSort::SortPairs(tmp, b2, reinterpret_cast<const uint32_t*>(cols), keys, iota,
                                   mem_e, (int)N, 0, bits, st);
@@ -348,13 +358,14 @@ static int bucket_sort_radix(const int32_t* cols, int64_t N, int32_t w, skb_ws* 
 
 // Stable counting sort of the n*s hash entries by bucket -> start[w+1], mem_e[N]
 // (entry indices, ascending within each bucket), plus a zeroed work counter.
-static int bucket_sort(const int32_t* cols, int64_t n, int32_t s, int32_t w, skb_ws* ws,
+static int bucket_sort(const int32_t* cols, const double* vals, int64_t n, int32_t s, int32_t w,
+                       skb_ws* ws,
                        cudaStream_t st, uint64_t** start_out, int32_t** mem_out,
                        unsigned int** counter_out) {
   const int64_t N = n * (int64_t)s;
   if ((N >= kRadixMinN || getenv("SKB_BUCKET_RADIX")) && N < (1ll << 31) &&
       !getenv("SKB_BUCKET_COUNTING"))
-    return bucket_sort_radix(cols, N, w, ws, st, start_out, mem_out, counter_out);
+    return bucket_sort_radix(cols, vals, N, w, ws, st, start_out, mem_out, counter_out);
   const int64_t C = std::max<int64_t>(4096, (N * (int64_t)w) / (16ll << 20) + 1);
   const int64_t nch = (N + C - 1) / C;
   int32_t* hist = (int32_t*)skb_ws_take(ws, (size_t)nch * w * 4);
@@ -380,7 +391,8 @@ static int bucket_sort(const int32_t* cols, int64_t n, int32_t s, int32_t w, skb
                            (int)csm);
       conf_sc = csm;
     }
-    bucket_scatter_kernel<<<(unsigned)nch, 256, csm, st>>>(cols, N, C, w, hist, start, mem_e);
+    bucket_scatter_kernel<<<(unsigned)nch, 256, csm, st>>>(cols, N, C, w, hist, start, vals,
+                                                           mem_e);
   }
   *start_out = start;
   *mem_out = mem_e;
@@ -418,7 +430,7 @@ __global__ void __launch_bounds__(32)
       int64_t c0 = 0, cnt = 0;
       double scl = 0.0, wv = 0.0;
       if (e < e1) {
-        const int64_t ei = mem_e[e];
+        const int64_t ei = (uint32_t)mem_e[e] & kMemIdx;
         const int64_t j = ei / s;
         wv = wvals[ei];
         scl = d[j];
@@ -476,10 +488,10 @@ __global__ void __launch_bounds__(kRmwThreads)
   const int rlo = (int)((int64_t)m * sl / S), rhi = (int)((int64_t)m * (sl + 1) / S);
   double* __restrict__ Xb = X + (int64_t)b * ldx;
   const uint64_t e0 = start[b], e1 = start[b + 1];
-  int64_t ei_next = e0 < e1 ? mem_e[e0] : 0;
+  int64_t ei_next = e0 < e1 ? ((uint32_t)mem_e[e0] & kMemIdx) : 0;
   for (uint64_t e = e0; e < e1; ++e) {
     const int64_t ei = ei_next;
-    if (e + 1 < e1) ei_next = mem_e[e + 1];
+    if (e + 1 < e1) ei_next = (uint32_t)mem_e[e + 1] & kMemIdx;
     const int64_t j = ei / s;
     const double wv = wvals[ei], dj = d[j];
     const int64_t c0 = colptr[j], c1 = colptr[j + 1];
@@ -538,7 +550,7 @@ __global__ void __launch_bounds__(kL2Threads)
     // pipeline registers: ei (chunk k+2), meta (chunk k+1), entries (chunk k)
     auto load_ei = [&](int k) -> int64_t {
       const int64_t e = e0 + 32 * (int64_t)k + lane;
-      return (k < nchunk && e < e1) ? (int64_t)ldg_ef(&mem_e[e], pol) : -1;
+      return (k < nchunk && e < e1) ? (int64_t)((uint32_t)ldg_ef(&mem_e[e], pol) & kMemIdx) : -1;
     };
     auto load_meta = [&](int64_t ei) -> L2Meta {
       L2Meta mt{0, 0, 0.0, 0.0};
@@ -635,19 +647,161 @@ __global__ void __launch_bounds__(kL2Threads)
   }
 }
 
+namespace skb {
+// ---- CSC A through ELL head records (m <= 65535): one CTA per bucket (dynamic
+// fetch), the bucket's row of X as an m-vector in shared memory. Members are
+// taken 256 at a time (one per thread, ascending j); each member's 64-byte
+// record (rows, values, and d_j written into it for this call) arrives in one
+// load, prefetched a batch ahead. The batch's terms fl(fl(A_ij d_j) v) are
+// added to the accumulator in rounds of bids (below), so each row takes its
+// terms in member order: every (row, bucket) sum is the reference's
+// ascending-j left-to-right fl-sum (bit-exact) with no
+// atomics on values. Columns longer than a record run member by member from
+// the CSC arrays (the batch is split there, order kept).
+constexpr int kEllSkT = 512;
+struct __align__(16) SkEll {  // = EllRec of skb_stream.cu, spare = d_j for this call
+  uint16_t row[5];
+  uint8_t cnt, pad[5];
+  double val[5];
+  double d;
+};
+static_assert(sizeof(SkEll) == 64, "ELL record");
+
+__global__ void ell_set_d_kernel(SkEll* __restrict__ ell, const double* __restrict__ d,
+                                 int64_t n) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) ell[j].d = d[j];
+}
+
+// Ordered application of one batch's terms without sorting: in round k every
+// pending term bids its member index for its row (shared atomicMin), the
+// lowest bidder of each row adds its term and resets the row's bid, the others
+// wait for the next round -- so each row receives its terms in ascending member
+// (= ascending j) order. Rounds = the largest multiplicity of a row in the
+// batch (~3 for 2,560 terms over 1e4 rows).
+__global__ void __launch_bounds__(kEllSkT, 1)
+    csc_sketch_ell_kernel(const SkEll* __restrict__ ell, const int64_t* __restrict__ colptr,
+                          const int32_t* __restrict__ rowidx, const double* __restrict__ av,
+                          const double* __restrict__ d, const uint64_t* __restrict__ start,
+                          const int32_t* __restrict__ mem_e, double vmag, int s, int w, int m,
+                          unsigned int* __restrict__ counter, double* __restrict__ X,
+                          int64_t ldx) {
+  __shared__ int sb, slong, spend;
+  extern __shared__ __align__(16) double acc[];  // m doubles, then m int32 bids
+  int* bid = reinterpret_cast<int*>(acc + m);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < m; i += kEllSkT) {
+    acc[i] = 0.0;
+    bid[i] = 0x7fffffff;
+  }
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) sb = (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int b = sb;
+    if (b >= w) break;
+    const uint64_t e0 = start[b], e1 = start[b + 1];
+    SkEll rec{};
+    uint32_t code = 0;
+    bool have = false;
+    auto fetch = [&](uint64_t eb) {
+      have = eb + tid < e1;
+      if (have) {
+        code = (uint32_t)mem_e[eb + tid];
+        const int64_t j = (int64_t)(code & 0x7FFFFFFFu) / s;
+        rec = ell[j];
+      }
+    };
+    fetch(e0);
+    for (uint64_t eb = e0; eb < e1; eb += kEllSkT) {
+      const SkEll r = rec;
+      const uint32_t c = code;
+      const bool h = have;
+      if (eb + kEllSkT < e1) fetch(eb + kEllSkT);  // next batch in flight during this one
+      const double v = (c & 0x80000000u) ? -vmag : vmag;
+      if (!__syncthreads_or(h && r.cnt > 5)) {
+        double t[5];
+        unsigned pend = 0;  // bit q: term q not applied yet
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          t[q] = __dmul_rn(__dmul_rn(r.val[q], r.d), v);
+          if (h && q < r.cnt) pend |= 1u << q;
+        }
+        while (__syncthreads_or(pend != 0)) {
+#pragma unroll
+          for (int q = 0; q < 5; ++q)
+            if (pend & (1u << q)) atomicMin(&bid[r.row[q]], tid);
+          __syncthreads();
+#pragma unroll
+          for (int q = 0; q < 5; ++q)
+            if ((pend & (1u << q)) && bid[r.row[q]] == tid) {
+              acc[r.row[q]] = __dadd_rn(acc[r.row[q]], t[q]);
+              pend &= ~(1u << q);
+              bid[r.row[q]] = 0x7fffffff;  // a member's rows are distinct: one reset each
+            }
+          __syncthreads();
+        }
+      } else {  // a long column in this batch: members one by one, in order
+        const int cnt = (int)min((uint64_t)kEllSkT, e1 - eb);
+        for (int q = 0; q < cnt; ++q) {
+          __syncthreads();
+          if (tid == q) sb = (int)c;  // broadcast the member code
+          __syncthreads();
+          const uint32_t cq = (uint32_t)sb;
+          const int64_t j = (int64_t)(cq & 0x7FFFFFFFu) / s;
+          const double vq = (cq & 0x80000000u) ? -vmag : vmag;
+          const double dj = d[j];
+          const int64_t a0 = colptr[j], a1 = colptr[j + 1];
+          for (int64_t e = a0 + tid; e < a1; e += kEllSkT) {  // a column's rows are distinct
+            const int row = rowidx[e];
+            acc[row] = __dadd_rn(acc[row], __dmul_rn(__dmul_rn(av[e], dj), vq));
+          }
+        }
+      }
+    }
+    __syncthreads();
+    double* xr = X + (int64_t)b * ldx;
+    for (int i = tid; i < m; i += kEllSkT) {
+      xr[i] = acc[i];
+      acc[i] = 0.0;
+    }
+  }
+}
+}  // namespace skb
+
 extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx,
-                                    const double* av, int64_t m, int64_t n, const double* d,
-                                    const int32_t* cols, const double* vals, int32_t s, int32_t w,
-                                    double* X, int64_t ldx, void* workspace, size_t ws_bytes,
-                                    void* stream) {
+                                    const double* av, void* ell, int64_t m, int64_t n,
+                                    const double* d, const int32_t* cols, const double* vals,
+                                    int32_t s, int32_t w, double* X, int64_t ldx,
+                                    void* workspace, size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (m < 1 || ldx < m || s < 1 || w < 1) return SKB_ERR_ARG;
   skb_ws ws = skb_ws_make(workspace, ws_bytes);
   uint64_t* start;
   int32_t* mem_e;
   unsigned int* counter;
-  int rc = bucket_sort(cols, n, s, w, &ws, st, &start, &mem_e, &counter);
+  int rc = bucket_sort(cols, vals, n, s, w, &ws, st, &start, &mem_e, &counter);
   if (rc) return rc;
+  if (ell && m > 2048 && m <= 65535 && n > 0 && !getenv("SKB_CSC_SKETCH_L2")) {
+    const size_t smem = (size_t)m * 12;  // accumulator + bids
+    static size_t conf_e = 0;
+    if (smem > conf_e) {
+      if (smem > 220 * 1024 ||
+          cudaFuncSetAttribute(csc_sketch_ell_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return SKB_ERR_UNSUPPORTED;
+      conf_e = smem;
+    }
+    // every hash value is +-1/sqrt(s) (skb_hash.cu: sign / sqrt(s), both correctly
+    // rounded, so the host's IEEE quotient is the same double)
+    const double vmag = 1.0 / std::sqrt((double)s);
+    ell_set_d_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((SkEll*)ell, d, n);
+    const int grid = std::min(skb_num_sms(), (int)w);
+    csc_sketch_ell_kernel<<<grid, kEllSkT, smem, st>>>((const SkEll*)ell, colptr, rowidx, av, d,
+                                                       start, mem_e, vmag, s, w, (int)m, counter,
+                                                       X, ldx);
+    return skb_launch_status(__func__);
+  }
   if (m > 2048 && !getenv("SKB_CSC_SKETCH_RMW")) {
     cudaMemsetAsync(X, 0, (size_t)w * ldx * 8, st);
     static const int l2cps = getenv("SKB_L2_CPS") ? atoi(getenv("SKB_L2_CPS")) : 2;
@@ -691,7 +845,7 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
   int32_t* mem_e;
   unsigned int* counter;
   {
-    int rc0 = bucket_sort(cols, n, s, w, &ws, st, &start, &mem_e, &counter);
+    int rc0 = bucket_sort(cols, vals, n, s, w, &ws, st, &start, &mem_e, &counter);
     if (rc0) return rc0;
   }
   const size_t col_bytes = (size_t)lda * 8;

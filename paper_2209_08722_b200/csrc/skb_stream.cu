@@ -903,11 +903,26 @@ namespace skb {
 // (Gathering z through L1 to fit two 1024-thread CTAs doubled the time.)
 constexpr int kCscThreads = 1024;
 
-template <class Op>
+// ELL head records (skb_csc_ell_build, once per matrix): 64 bytes per column
+// holding its first kEll rows (u16) and values, the count in byte 10 (255:
+// longer column, read from the CSC arrays). Thread j's record is one
+// contiguous 64-byte load independent of colptr: the dependent
+// colptr -> rowidx -> z chain of the plain CSC walk disappears.
+constexpr int kEll = 5;
+struct __align__(16) EllRec {
+  uint16_t row[kEll];
+  uint8_t cnt, pad[5];
+  double val[kEll];
+  int64_t spare;
+};
+static_assert(sizeof(EllRec) == 64, "ELL record");
+
+template <class Op, bool ELL>
 __global__ void __launch_bounds__(kCscThreads)
     csc_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
-               const double* __restrict__ vals, int m, int64_t n, const double* __restrict__ z,
-               double* __restrict__ part, Op op, const int* __restrict__ gate) {
+               const double* __restrict__ vals, const EllRec* __restrict__ ell, int m, int64_t n,
+               const double* __restrict__ z, double* __restrict__ part, Op op,
+               const int* __restrict__ gate) {
   if (gate && *gate) return;
   extern __shared__ __align__(16) double csm[];
   double* zs = csm;
@@ -923,6 +938,25 @@ __global__ void __launch_bounds__(kCscThreads)
 #pragma unroll
     for (int q = 0; q < 6; ++q) p.v[q] = 0.0;
     op.load(j, p);
+    if (ELL) {
+      const EllRec r = ell[j];
+      if (r.cnt <= kEll) {
+        double dot = 0.0;
+        if (Op::kDot) {
+#pragma unroll
+          for (int q = 0; q < kEll; ++q)
+            if (q < r.cnt) dot = fma(r.val[q], zs[r.row[q]], dot);
+        }
+        const double cf = op.coef(j, p, dot);
+        op.emit(j, p, dot, cf);
+        if (Op::kAxpy) {
+#pragma unroll
+          for (int q = 0; q < kEll; ++q)
+            if (q < r.cnt) atomicAdd(&us[r.row[q]], cf * r.val[q]);
+        }
+        continue;
+      }
+    }
     const int64_t e0 = colptr[j], e1 = colptr[j + 1];
     double dot = 0.0;
     if (Op::kDot)
@@ -940,7 +974,8 @@ __global__ void __launch_bounds__(kCscThreads)
 template <class Op>
 static int run_csc(const int64_t* colptr, const int32_t* rowidx, const double* vals, int m,
                    int64_t n, const double* z, double* out, const double* sub, const Op& op,
-                   skb_ws* ws, cudaStream_t st, const int* gate = nullptr) {
+                   skb_ws* ws, cudaStream_t st, const int* gate = nullptr,
+                   const void* ell = nullptr) {
   if (m < 1 || n < 0) return SKB_ERR_ARG;
   const size_t smem = (size_t)((Op::kDot ? m : 0) + (Op::kAxpy ? m : 0)) * 8;
   if (smem > 220 * 1024) return SKB_ERR_UNSUPPORTED;  // m <= 14080 with both vectors
@@ -954,16 +989,17 @@ static int run_csc(const int64_t* colptr, const int32_t* rowidx, const double* v
     part = (double*)skb_ws_take(ws, (size_t)grid * m * 8);
     if (!part) return SKB_ERR_WORKSPACE;
   }
-  auto kern = csc_kernel<Op>;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  auto kern = ell ? csc_kernel<Op, true> : csc_kernel<Op, false>;
+  static size_t configured[2] = {0, 0};
+  if (smem > 48 * 1024 && smem > configured[ell ? 1 : 0]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return SKB_ERR_CUDA;
-    configured = smem;
+    configured[ell ? 1 : 0] = smem;
   }
   if (n > 0)
-    kern<<<grid, thr, smem, st>>>(colptr, rowidx, vals, m, n, z, part, op, gate);
+    kern<<<grid, thr, smem, st>>>(colptr, rowidx, vals, (const EllRec*)ell, m, n, z, part, op,
+                                  gate);
   if (Op::kAxpy)
     reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, n > 0 ? grid : 0, m, sub, out,
                                                           gate);
@@ -999,7 +1035,7 @@ extern "C" int skb_csc_to_dense(const int64_t* colptr, const int32_t* rowidx, co
 #define SKB_CSC const int64_t *colptr, const int32_t *rowidx, const double *vals, int64_t m, \
                 int64_t n
 #define SKB_CSCP const int64_t *colptr, const int32_t *rowidx, const double *vals, \
-                 const void *plan, int64_t plan_chunks, int64_t m, int64_t n
+                 const void *plan, int64_t plan_chunks, const void *ell, int64_t m, int64_t n
 // the planned kernel when a plan is given (and applies), else the thread-per-column one
 #define SKB_CSC_RUN(Z, OUT, SUB, GATE)                                                      \
   do {                                                                                      \
@@ -1007,7 +1043,7 @@ extern "C" int skb_csc_to_dense(const int64_t* colptr, const int32_t* rowidx, co
     if (cscp_view(plan, plan_chunks, m, &pv))                                               \
       return run_cscp(pv, (int)m, Z, OUT, SUB, op, &ws, (cudaStream_t)stream, GATE);        \
     return run_csc(colptr, rowidx, vals, (int)m, n, Z, OUT, SUB, op, &ws,                   \
-                   (cudaStream_t)stream, GATE);                                             \
+                   (cudaStream_t)stream, GATE, ell);                                        \
   } while (0)
 
 extern "C" int skb_csc_normal_apply(SKB_CSCP, const double* d2, const double* z, double* u,
@@ -1041,12 +1077,51 @@ extern "C" int skb_csc_rhs(SKB_CSCP, const double* x, const double* s, const dou
   SKB_CSC_RUN(nullptr, p, r_p, nullptr);
 }
 
-extern "C" int skb_csc_gemv_t(SKB_CSC, const double* y, const double* add, const double* sub,
+extern "C" int skb_csc_gemv_t(SKB_CSCP, const double* y, const double* add, const double* sub,
                               double* t, void* workspace, size_t ws_bytes, void* stream) {
   SKB_WS;
+  (void)plan;
+  (void)plan_chunks;
   OpGemvT op{add, sub, t};
   return run_csc(colptr, rowidx, vals, (int)m, n, y, nullptr, nullptr, op, &ws,
-                 (cudaStream_t)stream);
+                 (cudaStream_t)stream, nullptr, ell);
+}
+
+namespace skb {
+__global__ void ell_build_kernel(const int64_t* __restrict__ colptr,
+                                 const int32_t* __restrict__ rowidx,
+                                 const double* __restrict__ vals, int64_t n,
+                                 EllRec* __restrict__ ell) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t e0 = colptr[j], e1 = colptr[j + 1];
+  EllRec r{};
+  const int64_t len = e1 - e0;
+  r.cnt = len <= kEll ? (uint8_t)len : (uint8_t)255;
+  for (int q = 0; q < kEll && q < len; ++q) {
+    r.row[q] = (uint16_t)rowidx[e0 + q];
+    r.val[q] = vals[e0 + q];
+  }
+  r.spare = e0;
+  ell[j] = r;
+}
+}  // namespace skb
+
+// ELL head records of a CSC matrix (m <= 65535): 64 bytes per column, built
+// once per matrix; passed as `ell` to the CSC passes. 0 when not applicable.
+extern "C" size_t skb_csc_ell_bytes(int64_t m, int64_t n) {
+  return (m >= 1 && m <= 65535 && n >= 1) ? (size_t)n * sizeof(skb::EllRec) : 0;
+}
+
+extern "C" int skb_csc_ell_build(const int64_t* colptr, const int32_t* rowidx, const double* vals,
+                                 int64_t m, int64_t n, void* ell, size_t ell_bytes,
+                                 void* stream) {
+  const size_t need = skb_csc_ell_bytes(m, n);
+  if (!need) return SKB_ERR_UNSUPPORTED;
+  if (!ell || ell_bytes < need || ((uintptr_t)ell & 15)) return SKB_ERR_ARG;
+  skb::ell_build_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      colptr, rowidx, vals, n, (skb::EllRec*)ell);
+  return skb_launch_status(__func__);
 }
 
 extern "C" int skb_csc_directions(SKB_CSCP, const double* dy, const double* x, const double* s,

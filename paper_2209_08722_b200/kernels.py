@@ -116,7 +116,22 @@ class SparseDeviceMatrix:
         passes (csrc/skb_cscplan.cuh) when one was built, else (None, 0): the
         thread-per-column passes with shared-memory atomics."""
         plan, nch = getattr(self, "_plan", None) or self.plan()
-        return (self.colptr, self.rowidx, self.vals, plan, nch, self.m, self.n)
+        return (self.colptr, self.rowidx, self.vals, plan, nch, self.ell(), self.m, self.n)
+
+    def ell(self):
+        """ELL head records (skb_csc_ell_build, one 64-byte record per column),
+        built once per matrix; None where they do not apply (m > 65535) or when
+        SKB_CSC_ELL=0."""
+        if not hasattr(self, "_ell"):
+            import os
+            self._ell = None
+            nb = int(_lib.lib().skb_csc_ell_bytes(self.m, self.n)) if self.n > 0 else 0
+            if nb > 0 and os.environ.get("SKB_CSC_ELL", "1") != "0":
+                buf = torch.empty(nb, dtype=torch.uint8, device=self.vals.device)
+                _lib.call("skb_csc_ell_build", self.colptr, self.rowidx, self.vals, self.m,
+                          self.n, buf, nb, stream_ptr())
+                self._ell = buf
+        return self._ell
 
     def plan(self, force: bool = False):
         """Build (once) the pass plan of the deterministic CSC passes: on
@@ -202,7 +217,7 @@ def rhs(A, x, s, sigma_mu: float, out, r_d=None, r_p=None):
 def gemv_t(A, y, out, add=None, sub=None):
     """out = (A' y [+ add]) [- sub]   (ipm_core.py:100,218)."""
     ws, cap = _ws(A.m)
-    pre, args = _amat(A, planned=False)
+    pre, args = _amat(A)
     _lib.call(pre + "gemv_t", *args, y, _p(add), _p(sub), out, ws, cap, stream_ptr())
     return out
 

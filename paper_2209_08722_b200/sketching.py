@@ -227,7 +227,8 @@ def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = 
         need = int(_lib.lib().skb_sketch_workspace_bytes(A.n, W.w, W.s))
         ws, cap = workspace(need)
         if lp.sparse:  # CSC A (config c4)
-            _lib.call("skb_csc_sketch_apply", *A.args(), d, W.cols, W.vals, W.s, W.w, X, ldx, ws,
+            _lib.call("skb_csc_sketch_apply", A.colptr, A.rowidx, A.vals, A.ell(), A.m, A.n, d,
+                      W.cols, W.vals, W.s, W.w, X, ldx, ws,
                       cap, stream_ptr())
         else:
             _lib.call("skb_sketch_apply", A.cols, m, A.n, A.lda, d, W.cols, W.vals, W.s, W.w, X,

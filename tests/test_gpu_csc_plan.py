@@ -54,8 +54,12 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("variant", ["plan", "ell", "plain"])
 @pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
-def test_planned_passes(K, name, make):
+def test_planned_passes(K, name, make, variant):
+    """variant: plan = the deterministic planned passes (+ ELL records for A'y);
+    ell = the atomic passes reading 64-byte ELL records; plain = the atomic
+    passes walking colptr -> rowidx -> vals."""
     A = make()
     m, n = A.shape
     g = np.random.Generator(np.random.Philox(8))
@@ -64,10 +68,18 @@ def test_planned_passes(K, name, make):
     x, s, c = g.random(n) + 0.2, g.random(n) + 0.2, g.standard_normal(n)
     v = 1e-3 * g.standard_normal(n)
     Ad = K.SparseDeviceMatrix.from_host(A)
-    plan, nch = Ad.plan(force=True)
-    assert plan is not None and nch > 0, "the plan applies to every case here"
+    if variant == "plan":
+        plan, nch = Ad.plan(force=True)
+        assert plan is not None and nch > 0, "the plan applies to every case here"
+    else:
+        Ad._plan, nch = (None, 0), 0
+        if variant == "plain":
+            Ad._ell = None
+        else:
+            assert Ad.ell() is not None
     Af = K.SparseDeviceMatrix.from_host(A)
     Af._plan = (None, 0)  # the thread-per-column atomic kernel
+    Af._ell = None
     u1 = torch.empty(m, dtype=torch.float64, device="cuda")
     u2 = torch.empty_like(u1)
     # normal operator vs scipy (float64) and vs the atomic kernel
@@ -77,12 +89,13 @@ def test_planned_passes(K, name, make):
     err = np.max(np.abs(_h(u1) - ref) / scale)
     K.normal_apply(Af, _t(d * d), _t(z), u2)
     err2 = np.max(np.abs(_h(u1) - _h(u2)) / scale)
-    print(f"{name}: m={m} n={n} nnz={A.nnz} chunks={nch} normal err {err:.2e} vs atomic {err2:.2e}")
+    print(f"{name}/{variant}: m={m} n={n} nnz={A.nnz} chunks={nch} normal err {err:.2e} "
+          f"vs atomic {err2:.2e}")
     assert err <= 1e-13 and err2 <= 1e-13
-    # bitwise deterministic run to run
-    for _ in range(3):
-        K.normal_apply(Ad, _t(d * d), _t(z), u2)
-        assert torch.equal(u1, u2)
+    if variant == "plan":  # bitwise deterministic run to run
+        for _ in range(3):
+            K.normal_apply(Ad, _t(d * d), _t(z), u2)
+            assert torch.equal(u1, u2)
     # gated launch is a no-op
     gate = torch.ones(1, dtype=torch.int32, device="cuda")
     u2.fill_(7.0)

@@ -89,22 +89,39 @@ def test_csc_sketch_apply_bit_exact(K):
     assert np.array_equal(_h(X.cols)[:, :3000].T, ref)
 
 
+@pytest.mark.parametrize("kernel", ["ell", "l2"])
 @pytest.mark.parametrize("m,n,k,w,s,radix", [(2500, 10_000, 5, 600, 4, False),
                                               (2600, 8000, 12, 500, 3, False),
-                                              (2500, 10_000, 5, 600, 4, True)])
-def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix):
+                                              (2500, 10_000, 5, 600, 4, True),
+                                              (2500, 10_000, 0, 700, 4, False)])
+def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix, kernel):
     """m > 2048 takes the warp-per-bucket L2 kernel: few buckets (many repeated
     rows per member chunk -> the ordered path) and columns longer than its
     8-entry register window (k = 12 -> the lane-by-lane path), bit-exact
     against the C restatement of scipy's summation order. radix: the bucket
     order from the CUB radix sort (its default from 2^20 entries, forced here)
-    instead of the counting sort."""
+    instead of the counting sort. kernel: the ELL-record kernel (one CTA per
+    bucket, radix-sorted batches; k = 0: ragged columns of 0..12 entries, the long
+    ones split a batch) or the L2 kernel (SKB_CSC_SKETCH_L2=1)."""
     from paper_2209_08722_b200 import sketching as S
     from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
     if radix:
         monkeypatch.setenv("SKB_BUCKET_RADIX", "1")
-    lpd = sparse_wide_lp(m, n, k, m + k)
+    if kernel == "l2":
+        monkeypatch.setenv("SKB_CSC_SKETCH_L2", "1")
+    if k == 0:  # ragged: mostly short columns, some longer than an ELL record
+        g0 = np.random.Generator(np.random.Philox(m + n))
+        lens = np.where(g0.random(n) < 0.9, g0.integers(0, 6, n), g0.integers(6, 13, n))
+        rows = [np.sort(g0.choice(m, size=int(c), replace=False)) for c in lens]
+        ptr = np.concatenate([[0], np.cumsum(lens)])
+        Asp = sp.csc_matrix((g0.standard_normal(int(ptr[-1])), np.concatenate(rows), ptr),
+                            shape=(m, n))
+        lpd = sparse_wide_lp(m, n, 5, m)
+        lpd.A = Asp
+    else:
+        lpd = sparse_wide_lp(m, n, k, m + k)
     lp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c))
+    assert (lp.A.ell() is not None)
     d = 10.0 ** np.random.Generator(np.random.Philox(m)).uniform(-3, 3, lpd.n)
     W = S.build_sparse_embedding(lpd.n, w, s, 90 + k)
     X = S.apply_sketch(lp, _t(d), W)

@@ -19,6 +19,9 @@ colptr = torch.arange(0, n * k + 1, k, dtype=torch.int64, device="cuda")
 A = K.SparseDeviceMatrix(colptr, rows, vals, m)
 B = K.SparseDeviceMatrix(colptr, rows, vals, m)
 B._plan = (None, 0)
+Cm = K.SparseDeviceMatrix(colptr, rows, vals, m)
+Cm._plan = (None, 0)
+Cm._ell = None
 d2 = torch.rand(n, dtype=F64, device="cuda", generator=g) + 0.5
 z = torch.randn(m, dtype=F64, device="cuda", generator=g)
 u = torch.empty(m, dtype=F64, device="cuda")
@@ -27,7 +30,7 @@ A.plan(force=True)
 torch.cuda.synchronize()
 print(f"plan build {1e3 * (time.perf_counter() - t0):.1f} ms, chunks {A.plan()[1]}")
 byt = 12 * n * k + 16 * n + 8 + 16 * m
-for name, M in (("planned", A), ("atomic", B)):
+for name, M in (("planned", A), ("atomic+ell", B), ("atomic", Cm)):
     for _ in range(3):
         K.normal_apply(M, d2, z, u)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
