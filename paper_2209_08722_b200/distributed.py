@@ -246,11 +246,23 @@ class Comm:
         return vals
 
     def gather_columns(self, t: torch.Tensor, n: int) -> torch.Tensor:
-        """All-gather the per-rank slices of an n-vector into the full vector."""
+        """All-gather the per-rank slices of an n-vector into the full vector
+        (contiguous blocks in rank order, of any sizes: the phase-1 auxiliary LP
+        puts its identity columns on the last rank)."""
         if self.world == 1:
             return t
-        sizes = [shard_range(n, r, self.world) for r in range(self.world)]
-        width = max(j1 - j0 for j0, j1 in sizes)
+        loc = torch.tensor([t.numel()], dtype=torch.int64,
+                           device="cpu" if self.host_staging else t.device)
+        lens = [torch.empty_like(loc) for _ in range(self.world)]
+        dist.all_gather(lens, loc, group=self.group)
+        lens = [int(v.item()) for v in lens]
+        assert sum(lens) == n, (lens, n)
+        sizes = []
+        j = 0
+        for ln in lens:
+            sizes.append((j, j + ln))
+            j += ln
+        width = max(lens)
         dev = "cpu" if self.host_staging else t.device
         buf = torch.zeros(width, dtype=t.dtype, device=dev)
         buf[: t.numel()].copy_(t)

@@ -215,14 +215,17 @@ def apply_sketch(lp, d: torch.Tensor, W: SketchOperator, check_positive: bool = 
     m = A.m
     ldx = lda_for(m)
     X = torch.empty((W.w, ldx), dtype=F64, device=d.device)
-    if W.kind == "identity":
-        Ad = lp.dense_A()
+    if W.kind == "identity":  # ADW = AD: X's rows are the scaled columns (w = n)
         if lp.comm.active:
             X.zero_()
-            sub = X[lp.j0:lp.j0 + A.n]
-            _lib.call("skb_scale_columns", Ad.cols, m, Ad.n, Ad.lda, d, sub, ldx, stream_ptr())
+        sub = X[lp.j0:lp.j0 + A.n] if lp.comm.active else X
+        if lp.sparse:  # scatter the CSC columns straight into X (A is never densified)
+            if not lp.comm.active:
+                X.zero_()
+            _lib.call("skb_csc_to_dense", A.colptr, A.rowidx, A.vals, A.n, sub, ldx, stream_ptr())
+            sub[:, :m] *= d[:, None]  # X[j, i] = A_ij * d_j, one rounding as in skb_scale_columns
         else:
-            _lib.call("skb_scale_columns", Ad.cols, m, Ad.n, Ad.lda, d, X, ldx, stream_ptr())
+            _lib.call("skb_scale_columns", A.cols, m, A.n, A.lda, d, sub, ldx, stream_ptr())
     elif W.kind == "sparse_sign":
         need = int(_lib.lib().skb_sketch_workspace_bytes(A.n, W.w, W.s))
         ws, cap = workspace(need)

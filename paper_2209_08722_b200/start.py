@@ -17,7 +17,7 @@ import scipy.sparse as sp
 import torch
 
 from . import _lib
-from .distributed import MIN, SUM
+from .distributed import MIN, SUM  # noqa: F401
 from .errors import DegenerateRow, Infeasible, InvariantViolated, MaxIterations
 from .errors import NeighborhoodViolated, NotPositiveDefinite, Unbounded
 from .lp_model import DeviceLP, LinearProgram, reduce_call
@@ -36,9 +36,15 @@ def _sub_params(params, **overrides):
 
 def phase1_lp(lp: DeviceLP):
     """min 1'z s.t. A_f x + z = b_f, (x, z) >= 0 with rows sign-flipped so b_f > 0
-    (lp_model.py:206-239). Returns (aux DeviceLP, start iterate)."""
+    (lp_model.py:206-239). Returns (aux DeviceLP, start iterate).
+
+    The auxiliary matrix [A_f, I] keeps A's storage: a CSC A gets a CSC
+    auxiliary (A's entries, sign-flipped, then one entry per identity column --
+    never densified), a dense A a column-major copy. Under column sharding each
+    rank keeps its block of A_f and the m identity columns go to the last rank,
+    so rank blocks stay contiguous and in order."""
     from .ipm_core import make_iterate
-    from .kernels import DeviceMatrix
+    from .kernels import DeviceMatrix, SparseDeviceMatrix
     b = lp.b
     sign = torch.where(b < 0, -1.0, 1.0).to(F64)
     bf = sign * b
@@ -46,20 +52,46 @@ def phase1_lp(lp: DeviceLP):
     if zero.numel():
         raise DegenerateRow(int(zero[0, 0].item()))
     m, n = lp.m, lp.n
-    if lp.comm.active:
-        raise NotImplementedError("phase 1 on a column-sharded LP")
-    lda = lp.A.lda
-    cols = torch.zeros((n + m, lda), dtype=F64, device=lp.device)
-    cols[:n, :m].copy_(lp.dense_A().cols[:, :m] * sign[None, :])  # A_f = diag(sign) A
-    cols[n + torch.arange(m, device=lp.device), torch.arange(m, device=lp.device)] = 1.0
-    Aaux = DeviceMatrix(cols, m)
-    c_aux = torch.cat([torch.zeros(n, dtype=F64, device=lp.device),
-                       torch.ones(m, dtype=F64, device=lp.device)])
-    aux = DeviceLP.from_device(Aaux, bf.contiguous(), c_aux, n + m, name=lp.name + "_phase1")
+    dev = lp.device
+    comm = lp.comm
+    last = comm.rank == comm.world - 1
+    nl = lp.n_local
+    nid = m if last else 0                      # identity columns held here
+    if lp.sparse:
+        A = lp.A
+        base = A.colptr[0]
+        cp = A.colptr - base
+        nnz = int(cp[-1].item())
+        rows = A.rowidx[int(base.item()):int(base.item()) + nnz]
+        vals = A.vals[int(base.item()):int(base.item()) + nnz] * sign[rows.long()]
+        if nid:
+            cp = torch.cat([cp, nnz + torch.arange(1, m + 1, dtype=torch.int64, device=dev)])
+            rows = torch.cat([rows, torch.arange(m, dtype=torch.int32, device=dev)])
+            vals = torch.cat([vals, torch.ones(m, dtype=F64, device=dev)])
+        Aaux = SparseDeviceMatrix(cp.contiguous(), rows.contiguous(), vals.contiguous(), m)
+        Af = A  # A_f 1 = sign .* (A 1): the row sign is applied to the sums below
+    else:
+        lda = lp.A.lda
+        cols = torch.zeros((nl + nid, lda), dtype=F64, device=dev)
+        cols[:nl, :m].copy_(lp.A.cols[:, :m] * sign[None, :])  # A_f = diag(sign) A
+        if nid:
+            cols[nl + torch.arange(m, device=dev), torch.arange(m, device=dev)] = 1.0
+        Aaux = DeviceMatrix(cols, m)
+        Af = DeviceMatrix(cols[:nl], m)
+    c_aux = torch.cat([torch.zeros(nl, dtype=F64, device=dev),
+                       torch.ones(nid, dtype=F64, device=dev)])
+    aux = DeviceLP.from_device(Aaux, bf.contiguous(), c_aux, n + m, j0=lp.j0, comm=comm,
+                               name=lp.name + "_phase1")
     from . import kernels as K
-    ones = torch.ones(n, dtype=F64, device=lp.device)
-    row_sums = torch.empty(m, dtype=F64, device=lp.device)
-    K.gemv(DeviceMatrix(cols[:n], m), ones, row_sums)              # A_f 1
+    ones = torch.ones(nl, dtype=F64, device=dev)
+    row_sums = torch.empty(m, dtype=F64, device=dev)
+    if nl > 0:
+        K.gemv(Af, ones, row_sums)                                   # A_f 1 (local block)
+    else:
+        row_sums.zero_()
+    if lp.sparse:
+        row_sums = row_sums * sign
+    comm.allreduce_(row_sums)
     top = float(row_sums.max().item())
     eps = float(bf.min().item() / (2.0 * top)) if top > 0 else 1.0
     bh, rh = bf.cpu().numpy(), row_sums.cpu().numpy()
@@ -71,6 +103,23 @@ def phase1_lp(lp: DeviceLP):
     y = np.zeros(m)
     s = np.maximum(np.concatenate([np.zeros(n), np.ones(m)]) + 1.0, 1.0)
     return aux, make_iterate(aux, x, y, s)
+
+
+def _pcg_solve_aat(lp: DeviceLP, rhs: torch.Tensor, params) -> torch.Tensor:
+    """(A A')^-1 rhs without forming A A' (sparse or sharded A): PCG on the
+    normal operator with D = I, preconditioned by the sketched factor of A
+    itself -- the hot path with d = 1 -- to 1e-14 relative."""
+    from .ipm_core import _build_factor
+    from .krylov_solvers import NormalOperator, pcg
+    from .sketching import auto_sketch_dims
+    ones = torch.ones(lp.n_local, dtype=F64, device=lp.device)
+    op = NormalOperator(lp, ones, check=False)
+    w, s_nnz = auto_sketch_dims(lp.m, lp.n, params.delta)
+    w = min(lp.n, max(4 * lp.m, min(w, 8 * lp.m)))
+    rng = np.random.Generator(np.random.Philox(int(params.seed) + 0x5EED))
+    W, factor, _ = _build_factor(lp, ones, params, rng, w, max(4, min(s_nnz, 8)))
+    y, trace = pcg(op, factor, rhs, max(200, 4 * lp.m), 1e-14)
+    return y
 
 
 def _chol_solve_aat(lp: DeviceLP, rhs: torch.Tensor) -> torch.Tensor:
@@ -108,19 +157,32 @@ def phase1_point(lp: DeviceLP, params):
     z_sum = float(np.sum(rep.x[lp.n:]))
     if z_sum > 1e-7 * (1.0 + lp.b_norm):
         raise Infeasible(f"phase-1 optimum 1'z = {z_sum:.3e} is bounded away from zero")
-    x0 = torch.from_numpy(np.ascontiguousarray(rep.x[:lp.n])).to(lp.device)
-    Ad = lp.dense_A()
-    _lib.call("skb_zero_col_fill", Ad.cols, lp.m, Ad.n, Ad.lda, x0, stream_ptr())
+    x0 = lp.local(torch.from_numpy(np.ascontiguousarray(rep.x[:lp.n])).to(lp.device))
+    if lp.sparse:  # all-zero columns: x = 1 (ipm_core.py:831-832)
+        x0[(lp.A.colptr[1:] - lp.A.colptr[:-1]) == 0] = 1.0
+    elif lp.n_local > 0:
+        _lib.call("skb_zero_col_fill", lp.A.cols, lp.m, lp.A.n, lp.A.lda, x0, stream_ptr())
+    from .errors import Breakdown, RankDeficient
     try:
         resid = lp.gemv(x0, sub=lp.b)                 # A x0 - b
         resid.neg_()                                  # b - A x0
-        corr = lp.gemv_t(_chol_solve_aat(lp, resid))  # A' (A A')^-1 (b - A x0)
+        if lp.sparse or lp.comm.active:               # never densify A (c4) or gather it
+            y = _pcg_solve_aat(lp, resid, params)
+        else:
+            y = _chol_solve_aat(lp, resid)
+        corr = lp.gemv_t(y)                           # A' (A A')^-1 (b - A x0)
         cand = x0 + corr
-        if float(cand.min().item()) > 0:
+        cmin = torch.tensor([float(cand.min().item()) if cand.numel() else float("inf")],
+                            dtype=F64, device=lp.device)
+        lp.comm.allreduce_(cmin, MIN)
+        if float(cmin.item()) > 0:
             x0 = cand
-    except NotPositiveDefinite:
+    except (NotPositiveDefinite, Breakdown, RankDeficient):
         pass
-    if not float(x0.min().item()) > 0:
+    xmin = torch.tensor([float(x0.min().item()) if x0.numel() else float("inf")],
+                        dtype=F64, device=lp.device)
+    lp.comm.allreduce_(xmin, MIN)
+    if not float(xmin.item()) > 0:
         raise NeighborhoodViolated("phase-1 produced a boundary primal point")
     return x0, rep
 
@@ -210,7 +272,10 @@ def feasible_start(lp: DeviceLP, params):
         y_cand = torch.from_numpy(np.ascontiguousarray(rep.y)).to(lp.device)
         s_cand = lp.gemv_t(y_cand)                          # A' y
         s_cand = lp.c - s_cand                              # c - A' y
-        if float(s_cand.min().item()) >= 0.25 * delta:
+        smin = torch.tensor([float(s_cand.min().item()) if s_cand.numel() else float("inf")],
+                            dtype=F64, device=lp.device)
+        lp.comm.allreduce_(smin, MIN)
+        if float(smin.item()) >= 0.25 * delta:
             y0, s0 = y_cand, s_cand
             break
     if y0 is None:

@@ -252,6 +252,30 @@ def start_traces():
         json.dump(res, f)
 
 
+def start_sparse_traces():
+    """solve() with no start in feasible mode on a SPARSE LP (random_feasible_lp
+    at 2% fill: CSC on the device, ~30% empty columns -> the zero-column fill),
+    phase 1 and centering included (ipm_core.py:814-969)."""
+    res = {}
+    lp = skipm.random_feasible_lp(60, 4000, 0.02, 5)
+    prm = ipm_core.IpmParams(mode="feasible", gamma=0.5, sigma=0.5, tol_outer=1e-6, seed=4)
+    x0, aux = ipm_core.phase1_point(lp, prm)
+    res["phase1_x0"] = x0.tolist()
+    res["phase1_aux_outer"] = aux.outer
+    st = ipm_core.feasible_start(lp, prm)
+    res["start"] = dict(x=st.x.tolist(), y=st.y.tolist(), s=st.s.tolist(), mu=st.mu)
+    rep = ipm_core.solve(lp, None, prm)
+    d = rep.to_dict()
+    d.pop("params")
+    res["solve"] = d
+    res["lp"] = dict(m=60, n=4000, density=0.02, seed=5, nnz=int(lp.A.nnz),
+                     empty_cols=int((np.diff(lp.A.tocsc().indptr) == 0).sum()))
+    print(f"sparse feasible start: aux outer {aux.outer}, start mu {st.mu:.4e}, solve outer "
+          f"{rep.outer} obj {rep.objective!r}, empty cols {res['lp']['empty_cols']}")
+    with open(os.path.join(HERE, "start_sparse_traces.json"), "w") as f:
+        json.dump(res, f)
+
+
 def write_libsvm_sample(path):
     """A small synthetic LIBSVM file (seeded; comments, blank lines, a repeated
     index, unsorted indices) for the ingestion parity test."""
@@ -331,7 +355,7 @@ def lp_csr(lpd):
 
 if __name__ == "__main__":
     what = sys.argv[1:] or ["hashes", "adw", "small", "c1", "solvers", "start", "gaussian",
-                            "sparse", "svm", "diag"]
+                            "sparse", "svm", "diag", "start_sparse"]
     if "svm" in what:
         svm_traces()
     if "diag" in what:
@@ -342,6 +366,8 @@ if __name__ == "__main__":
         gaussian_traces()
     if "start" in what:
         start_traces()
+    if "start_sparse" in what:
+        start_sparse_traces()
     if "solvers" in what:
         solver_traces()
     if "hashes" in what:

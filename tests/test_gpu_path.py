@@ -471,6 +471,42 @@ def test_feasible_start_and_solve_without_start(P):
     assert abs(rep.objective - gs["objective"]) <= 1e-8 * abs(gs["objective"])
 
 
+def test_feasible_start_sparse_without_densifying(P, monkeypatch):
+    """No start, feasible mode, a SPARSE LP (CSC on the device, 1,149 empty
+    columns): phase 1 runs on a CSC auxiliary [A_f, I], the projection
+    A'(AA')^-1(b - A x0) by PCG on the D = I normal operator, and nothing ever
+    densifies A (dense_A is made to fail) -- the path c4 needs.
+    Compared with the live reference's own run (tests/golden/start_sparse_traces.json)."""
+    from paper_2209_08722_b200 import ipm_core as IC
+    from paper_2209_08722_b200.lp_model import DeviceLP
+    from paper_2209_08722_b200.lp_model import random_feasible_lp as rfl
+    with open(os.path.join(GOLDEN, "start_sparse_traces.json")) as f:
+        gold = json.load(f)
+
+    def no_dense(self):
+        raise AssertionError("the sparse start path densified A")
+    monkeypatch.setattr(DeviceLP, "dense_A", no_dense)
+    lp = rfl(60, 4000, 0.02, 5)
+    dlp = DeviceLP.from_host(lp)
+    assert dlp.sparse
+    prm = IC.IpmParams(mode="feasible", gamma=0.5, sigma=0.5, tol_outer=1e-6, seed=4)
+    x0, aux = IC.phase1_point(dlp, prm)
+    assert aux.outer == gold["phase1_aux_outer"]
+    g0 = np.array(gold["phase1_x0"])
+    dx = np.max(np.abs(x0 - g0)) / np.max(np.abs(g0))
+    st = IC.feasible_start(dlp, prm)
+    dmu = abs(st.mu - gold["start"]["mu"]) / gold["start"]["mu"]
+    rep = IC.solve(dlp, None, prm)
+    gs = gold["solve"]
+    print(f"sparse start: phase-1 x0 rel dev {dx:.2e}, start mu rel dev {dmu:.2e}, "
+          f"outer {rep.outer} (ref {gs['outer']})")
+    assert dx <= 1e-7 and dmu <= 1e-8
+    assert rep.outer == gs["outer"] and [r.inner_iterations for r in rep.steps] == \
+        gs["inner_iterations"]
+    np.testing.assert_allclose(rep.mu_trace, gs["mu_trace"], rtol=1e-6)
+    assert abs(rep.objective - gs["objective"]) <= 1e-8 * abs(gs["objective"])
+
+
 @pytest.mark.parametrize("name", ["chebyshev", "unpreconditioned", "direct", "pcg_nocorr"])
 def test_other_solvers_trajectories(P, monkeypatch, name):
     """The device Chebyshev / plain CG / direct solvers and correction-off PCG

@@ -109,6 +109,57 @@ def test_sharded_solve_matches_reference(world, kind):
     assert all(r[3] == res[0][3] for r in res)  # replicated scalars identical on every rank
 
 
+def _start_rank(rank, world, port, q):
+    """No-start feasible solve of a sparse LP, column-sharded: phase 1 with the
+    identity columns on the last rank, PCG projection, shifted dual, centering."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2209_08722_b200 import ipm_core as IC
+        from paper_2209_08722_b200.distributed import Comm
+        from paper_2209_08722_b200.lp_model import DeviceLP
+        from paper_2209_08722_b200.lp_model import random_feasible_lp as rfl
+        dlp = DeviceLP.from_host(rfl(60, 4000, 0.02, 5), comm=Comm())
+        prm = IC.IpmParams(mode="feasible", gamma=0.5, sigma=0.5, tol_outer=1e-6, seed=4)
+        rep = IC.solve(dlp, None, prm)
+        q.put((rank, rep.outer, [r.inner_iterations for r in rep.steps], rep.mu_trace,
+               rep.objective, rep.x.shape[0]))
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_solve_without_start_sparse():
+    """SURVEY.md §8(f)2 under sharding: the whole start construction on a
+    column-sharded sparse LP (world 2, gloo) against the reference's run."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    with open(os.path.join(GOLDEN, "start_sparse_traces.json")) as f:
+        gs = json.load(f)["solve"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_start_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=900) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+    assert all(r[1] != "error" for r in res), res
+    for rank, outer, inner, mu, obj, nx in res:
+        dev = np.max(np.abs(np.array(mu) - gs["mu_trace"]) / np.array(gs["mu_trace"]))
+        print(f"[sharded start rank {rank}] outer {outer} (ref {gs['outer']}), "
+              f"max mu rel dev {dev:.2e}")
+        assert nx == 4000 and outer == gs["outer"] and inner == gs["inner_iterations"]
+        assert dev <= 1e-6
+        assert abs(obj - gs["objective"]) <= 1e-8 * abs(gs["objective"])
+
+
 def _gauss_rank(rank, world, port, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
