@@ -460,15 +460,16 @@ SKB_DEV void leaf_inverse(const double (*Lsm)[LDP], const double* rinv, double* 
   }
 }
 
-__global__ void __launch_bounds__(kLeafThreads) potrf_diag_kernel(double* G, int64_t ld, int k0,
-                                                                   int nb, int* status,
-                                                                   double* Dinv) {
+// The 64 x 64 diagonal factor (+ inverse Dinv = L^-1, 64 x 64 row-major) of
+// the tile at src (ld), L written to dst (ld_dst; may alias src).
+SKB_DEV void diag_factor(const double* src, int64_t ld, double* dst, int64_t ld_dst, int* status,
+                         double* Dinv) {
   __shared__ double Lsm[NB][LDP];
   __shared__ double colc[2][NB];
   __shared__ double rinv[NB];
   __shared__ int bad_s;
   const int t = threadIdx.x, i = t >> 2, q4 = t & 3;
-  double* B = G + (int64_t)k0 * ld + k0;
+  const double* B = src;
   double r[16];  // r[j] = A[i][q4 + 4 (j + g)] in column group g
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(kLeafThreads) potrf_diag_kernel(double* G, int
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int k = q4 + 4 * j;
-    B[(int64_t)i * ld + k] = Lsm[i][k];
+    dst[(int64_t)i * ld_dst + k] = Lsm[i][k];
   }
   if (bad_s) {
     if (t == 0) atomicOr(status, ST_CHOL_FAIL);
@@ -517,6 +518,144 @@ __global__ void __launch_bounds__(kLeafThreads) potrf_diag_kernel(double* G, int
   if (!Dinv) return;
   leaf_inverse(Lsm, rinv, Dinv, NB);
 }
+
+
+__global__ void __launch_bounds__(kLeafThreads) potrf_diag_kernel(double* G, int64_t ld, int k0,
+                                                                   int nb, int* status,
+                                                                   double* Dinv) {
+  double* B = G + (int64_t)k0 * ld + k0;
+  diag_factor(B, ld, B, ld, status, Dinv);
+}
+
+// ---- fused right-looking step (one launch per 64-wide panel, nb <= kStepMax)
+// Step k runs one CTA per lower tile pair (i, j), k < j <= i < T: it forms the
+// panel tiles L_ik = A_ik Dinv_k' and L_jk (64^3 DMMA products from shared
+// memory), updates A_ij -= L_ik L_jk', CTA (i, k + 1) stores L_ik, and CTA
+// (k + 1, k + 1) -- the only one updating the next diagonal tile -- factors
+// that tile and inverts it for step k + 1 (Dinv ping-pongs between two
+// buffers). One launch per panel instead of three, and the next diagonal
+// factor overlaps the rest of the trailing update. Every product runs the
+// same DMMA k sequence (0, 4, ..., 60 from zero) and the same epilogue
+// rounding as the GEMM-based loop, so L is bitwise identical to it. L goes to
+// a separate buffer Lo (the panel's A tiles are still being read during the
+// step) and is copied back at the end.
+constexpr int kSLD = NB + 4;  // row stride = 4 (mod 16) doubles: conflict-free fragment reads
+
+SKB_DEV void tile_load(double* s, const double* g, int64_t ld) {
+  for (int e = threadIdx.x; e < NB * NB / 2; e += kLeafThreads) {
+    const int r = e >> 5, c = (e & 31) * 2;
+    *reinterpret_cast<double2*>(s + r * kSLD + c) =
+        *reinterpret_cast<const double2*>(g + (int64_t)r * ld + c);
+  }
+}
+
+// acc[a][b] (warp tile 32 x 16 at (wr * 32, wc * 16)) = sum_q sA[row][q] sB[col][q]
+SKB_DEV void tile_mm_nt(const double* sA, const double* sB, double (&acc)[4][2][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = warp >> 2, wc = warp & 3, gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < NB; kk += 4) {
+    double af[4], bf[2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) af[a] = sA[(wr * 32 + a * 8 + gq) * kSLD + kk + tq];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) bf[b] = sB[(wc * 16 + b * 8 + gq) * kSLD + kk + tq];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) dmma(acc[a][b], af[a], bf[b]);
+  }
+}
+
+SKB_DEV void tile_store_acc(double* s, const double (&acc)[4][2][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = warp >> 2, wc = warp & 3, gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+      *reinterpret_cast<double2*>(s + (wr * 32 + a * 8 + gq) * kSLD + wc * 16 + b * 8 + tq * 2) =
+          make_double2(acc[a][b][0], acc[a][b][1]);
+}
+
+__global__ void __launch_bounds__(kLeafThreads) potrf_step_kernel(double* G, int64_t ld,
+                                                                   double* Lo, int64_t ldo, int k,
+                                                                   double* Dbuf, int* status) {
+  extern __shared__ __align__(16) double psm[];
+  double* sAi = psm;
+  double* sAj = sAi + NB * kSLD;
+  double* sD = sAj + NB * kSLD;
+  int i = 0, j = 0;
+  if (k >= 0) {
+    const int p = blockIdx.x;
+    int ii = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
+    while ((ii + 1) * (ii + 2) / 2 <= p) ++ii;
+    while (ii * (ii + 1) / 2 > p) --ii;
+    i = k + 1 + ii;
+    j = k + 1 + (p - ii * (ii + 1) / 2);
+    const double* Dk = Dbuf + (k & 1) * NB * NB;
+    tile_load(sAi, G + (int64_t)i * NB * ld + (int64_t)k * NB, ld);
+    if (j != i) tile_load(sAj, G + (int64_t)j * NB * ld + (int64_t)k * NB, ld);
+    tile_load(sD, Dk, NB);
+    __syncthreads();
+    double acc[4][2][2], acc2[4][2][2];
+    tile_mm_nt(sAi, sD, acc);                      // L_ik = A_ik Dinv_k'
+    if (j != i) tile_mm_nt(sAj, sD, acc2);         // L_jk
+    __syncthreads();
+    tile_store_acc(sAi, acc);
+    if (j != i) tile_store_acc(sAj, acc2);
+    __syncthreads();
+    const double* sLj = j != i ? sAj : sAi;
+    if (j == k + 1) {  // the unique CTA of tile row i that stores L_ik
+      double* o = Lo + (int64_t)i * NB * ldo + (int64_t)k * NB;
+      for (int e = threadIdx.x; e < NB * NB / 2; e += kLeafThreads) {
+        const int r = e >> 5, c = (e & 31) * 2;
+        *reinterpret_cast<double2*>(o + (int64_t)r * ldo + c) =
+            *reinterpret_cast<const double2*>(sAi + r * kSLD + c);
+      }
+    }
+    tile_mm_nt(sAi, sLj, acc);                     // L_ik L_jk'
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wr = warp >> 2, wc = warp & 3, gq = lane >> 2, tq = lane & 3;
+    double* C = G + (int64_t)i * NB * ld + (int64_t)j * NB;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = wr * 32 + a * 8 + gq, c = wc * 16 + b * 8 + tq * 2 + q;
+          if (i != j || c <= r) {  // diagonal tiles: lower part only (upper stays zero)
+            double* dst = C + (int64_t)r * ld + c;
+            *dst = fma(1.0, *dst, -acc[a][b][q]);
+          }
+        }
+  }
+  if (i == k + 1 && j == k + 1) {  // the next diagonal tile: factor + invert it
+    __syncthreads();                 // this CTA's global writes are visible to it
+    const double* src = G + (int64_t)i * NB * ld + (int64_t)i * NB;
+    diag_factor(src, ld, Lo + (int64_t)i * NB * ldo + (int64_t)i * NB, ldo, status,
+                Dbuf + ((k + 1) & 1) * NB * NB);
+  }
+}
+
+// G[lower tiles] <- Lo (the strict upper part of the diagonal tiles is zero in Lo).
+__global__ void copy_lower_tiles_kernel(double* G, int64_t ld, const double* Lo, int64_t ldo,
+                                        int nb) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t half = (int64_t)nb * nb / 2;
+  if (idx >= half) return;
+  const int r = (int)(idx / (nb / 2)), c = (int)(idx % (nb / 2)) * 2;
+  if (c / NB > r / NB) return;
+  *reinterpret_cast<double2*>(G + (int64_t)r * ld + c) =
+      *reinterpret_cast<const double2*>(Lo + (int64_t)r * ldo + c);
+}
+
+constexpr size_t kStepSmem = (size_t)3 * NB * kSLD * sizeof(double);
 
 // Inverses of the 64 x 64 diagonal blocks of a lower-triangular L (one CTA
 // per block), with the row-parallel scheme of potrf_diag_kernel.
@@ -871,7 +1010,39 @@ extern "C" int32_t skb_factor_padded_dim(int32_t m) { return round_pad(m); }
 // Per 64-wide panel: diagonal factor + its inverse (one CTA), panel
 // L21 = A21 L11^-T as a DMMA GEMM (in place: each CTA owns whole rows),
 // trailing update A22 -= L21 L21' on the lower tiles.
+static int potrf_fused(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStream_t st) {
+  const size_t mark = ws->off;
+  double* Dbuf = (double*)skb_ws_take(ws, (size_t)2 * NB * NB * 8);
+  double* Lo = (double*)skb_ws_take(ws, (size_t)Mp * Mp * 8);
+  if (!Dbuf || !Lo) {
+    ws->off = mark;
+    return 1;
+  }
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(potrf_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kStepSmem);
+    configured = true;
+  }
+  const int T = Mp / NB;
+  potrf_step_kernel<<<1, kLeafThreads, kStepSmem, st>>>(G, ld, Lo, Mp, -1, Dbuf, status);
+  for (int k = 0; k + 1 < T; ++k) {
+    const int tp = T - 1 - k;
+    potrf_step_kernel<<<tp * (tp + 1) / 2, kLeafThreads, kStepSmem, st>>>(G, ld, Lo, Mp, k, Dbuf,
+                                                                          status);
+  }
+  const int64_t half = (int64_t)Mp * Mp / 2;
+  copy_lower_tiles_kernel<<<(unsigned)((half + 255) / 256), 256, 0, st>>>(G, ld, Lo, Mp, Mp);
+  ws->off = mark;
+  return skb_launch_status(__func__);
+}
+
 static int potrf(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, cudaStream_t st) {
+  const char* loop = getenv("SKB_POTRF_LOOP");  // per call: the tests compare both
+  if (!loop || !atoi(loop)) {
+    const int rc = potrf_fused(G, ld, Mp, status, ws, st);
+    if (rc <= 0) return rc;
+  }
   const size_t mark = ws->off;
   double* Dinv = (double*)skb_ws_take(ws, (size_t)NB * NB * 8);
   if (!Dinv) return SKB_ERR_WORKSPACE;

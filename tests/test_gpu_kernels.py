@@ -258,3 +258,37 @@ def test_potrf_trtri_against_numpy(K, monkeypatch, Mp, emu):
     _lib.call("skb_trtri", G, Li, Mp, Mp, ws, cap, stream_ptr())
     E = np.tril(_h(Li)) @ Lref - np.eye(Mp)
     assert np.max(np.abs(E)) <= 1e-9
+
+
+@pytest.mark.parametrize("Mp", [64, 192, 1024, 2048, 6144])
+def test_potrf_fused_steps_bitwise_equal_panel_loop(K, monkeypatch, Mp):
+    """The one-launch-per-panel Cholesky (potrf_step_kernel) against the
+    three-launch GEMM panel loop (SKB_POTRF_LOOP=1): same DMMA k sequence and
+    epilogue rounding, so L must be bitwise identical; a non-SPD input flags
+    the status word in both."""
+    from paper_2209_08722_b200 import _lib
+    from paper_2209_08722_b200.runtime import stream_ptr, workspace
+    monkeypatch.setenv("SKB_GEMM_EMU", "0")
+    g = np.random.Generator(np.random.Philox(Mp + 7))
+    X = g.standard_normal((Mp + 64, Mp))
+    S = np.tril(X.T @ X)
+    ws, cap = workspace(int(_lib.lib().skb_factor_workspace_bytes(Mp, Mp + 64)))
+    outs = {}
+    for loop in ("0", "1"):
+        monkeypatch.setenv("SKB_POTRF_LOOP", loop)
+        G = _t(S)
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.call("skb_potrf", G, Mp, Mp, st, ws, cap, stream_ptr())
+        assert int(st.item()) == 0
+        outs[loop] = _h(G)
+    assert np.array_equal(outs["0"], outs["1"])
+    assert np.array_equal(np.triu(outs["0"], 1), np.zeros((Mp, Mp)))
+    Lref = np.linalg.cholesky(X.T @ X)
+    assert np.max(np.abs(outs["0"] - Lref)) <= 1e-10 * np.abs(Lref).max()
+    bad = S.copy()
+    bad[Mp // 2, Mp // 2] = -1.0
+    for loop in ("0", "1"):
+        monkeypatch.setenv("SKB_POTRF_LOOP", loop)
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.call("skb_potrf", _t(bad), Mp, Mp, st, ws, cap, stream_ptr())
+        assert int(st.item()) & 4

@@ -38,3 +38,10 @@ def ygemm():
     _lib.call("skb_gemm", 0, 1, w, m, m, 1.0, X.cols, X.lda, Li, Mp, 0.0, Y, X.lda, 0, 1, 0, 0, 0, ws, cap, stream_ptr())
 print("Y = X Linv' ms", ev(ygemm))
 print("full factor ms", ev(lambda: PC.build_preconditioner(X), reps=3))
+f = PC.build_preconditioner(X)
+Linv = torch.empty_like(G); LinvT = torch.empty_like(G)
+stats = np.zeros(4)
+def cq2():
+    _lib.call("skb_factor_cholqr2", X.cols, X.lda, w, m, Linv, LinvT, None, stats.ctypes.data, ws, cap, stream_ptr())
+print("skb_factor_cholqr2 alone ms", ev(cq2, reps=5))
+print("rank_check alone ms", ev(lambda: PC.rank_check(f), reps=5))
