@@ -19,7 +19,8 @@ Cases (SURVEY.md §8(d) generators; gamma widened as in App. C):
   m2000     wide_dense_lp(2000, 100_000, 2),   w=8000, s=4, 6 steps (warp-pair K4)
   sparse1e4 sparse_wide_lp(10_000, 200_000, 5, 3), w=40_000, s=4, 3 steps
             (L2 CSC sketch, INT8-emulated factor GEMMs at m=1e4)
-  c5m1000   ill_conditioned_lp(1000, 100_000, 4), Gaussian w=4000, sigma=0.3, full solve
+  c5m1000   ill_conditioned_lp(1000, 20_000, 4), Gaussian w=4000, sigma=0.3, 6 steps
+            (scipy's sparse x dense AD @ W is single-threaded: ~1 min per sketch here)
 """
 
 from __future__ import annotations
@@ -53,8 +54,8 @@ CASES = {
                   sigma=0.5, tol=1e-8, steps=6, seed=2),
     "sparse1e4": dict(gen=("sparse", 10_000, 200_000, 3), w=40_000, sketch="sparse", s=(4,),
                       sigma=0.5, tol=1e-8, steps=3, seed=3),
-    "c5m1000": dict(gen=("ill", 1000, 100_000, 4), w=4000, sketch="gaussian", s=(0,),
-                    sigma=0.3, tol=1e-8, steps=None, seed=4),
+    "c5m1000": dict(gen=("ill", 1000, 20_000, 4), w=4000, sketch="gaussian", s=(0,),
+                    sigma=0.3, tol=1e-8, steps=6, seed=4),
 }
 
 

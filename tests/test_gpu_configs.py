@@ -18,7 +18,7 @@ prints the largest deviation it measured.
   m2000      2000 x 1e5 dense, w=8000, s=4: 6 steps (the warp-pair K4 kernel)
   sparse1e4  1e4 x 2e5 CSC (5 nnz/col), w=4e4, s=4: 3 steps (L2 CSC sketch,
              INT8-emulated factor GEMMs)
-  c5m1000    ill-conditioned 1000 x 1e5, Gaussian w=4000, sigma=0.3: whole solve
+  c5m1000    ill-conditioned 1000 x 2e4, Gaussian w=4000, sigma=0.3: 6 steps
 """
 
 import json
