@@ -80,6 +80,65 @@ SKB_DEV double zig_fast_value(const ZigTables& T, uint64_t r) {
   return ((r >> 8) & 1) ? -x : x;
 }
 
+// log1p(x) for x in (-1, 0], bit-identical to the host libm numpy calls in the
+// ziggurat tail (npy_log1p -> glibc 2.39 log1p). glibc's log1p is the fdlibm
+// algorithm (argument reduction to 1 + f, s = f / (2 + f), a degree-7 odd
+// polynomial in s evaluated in Estrin form), and on FMA-capable x86 hosts
+// glibc runs its FMA build of it: the contractions below are that build's
+// (checked bit for bit against glibc on 4e8 arguments, tests/golden/log1p_check.c).
+// CUDA's own log1p differs from it in the last place on ~0.4% of arguments.
+SKB_DEV double glibc_log1p(double x) {
+  constexpr double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  constexpr double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01,
+                   Lp3 = 2.857142874366239149e-01, Lp4 = 2.222219843214978396e-01,
+                   Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+                   Lp7 = 1.479819860511658591e-01;
+  const int hx = __double2hiint(x), ax = hx & 0x7fffffff;
+  if (ax >= 0x3ff00000) return x == -1.0 ? -INFINITY : __longlong_as_double(0x7ff8000000000000ll);
+  if (ax < 0x3e200000) return ax < 0x3c900000 ? x : __fma_rn(-__dmul_rn(x, x), 0.5, x);
+  int k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx <= (int)0xbfd2bec3) {  // -0.2929 < x <= 0 (x is never positive here)
+    k = 0;
+    f = x;
+    hu = 1;
+  } else {
+    double u = __dadd_rn(1.0, x);
+    hu = __double2hiint(u);
+    k = (hu >> 20) - 1023;
+    c = k > 0 ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+    c = __ddiv_rn(c, u);
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = __hiloint2double(hu | 0x3ff00000, __double2loint(u));
+    } else {
+      k += 1;
+      u = __hiloint2double(hu | 0x3fe00000, __double2loint(u));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+  const double kd = (double)k;
+  if (hu == 0) {
+    if (f == 0.0) return k == 0 ? 0.0 : __fma_rn(kd, ln2_hi, __fma_rn(kd, ln2_lo, c));
+    const double R = __dmul_rn(hfsq, __fma_rn(-0.66666666666666666, f, 1.0));
+    if (k == 0) return __dsub_rn(f, R);
+    return __fma_rn(kd, ln2_hi, -__dsub_rn(__dsub_rn(R, __fma_rn(kd, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+  const double z = __dmul_rn(s, s);
+  const double R2 = __fma_rn(Lp3, z, Lp2), R3 = __fma_rn(Lp5, z, Lp4), R4 = __fma_rn(Lp7, z, Lp6);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z4, z2);
+  double R = __fma_rn(z, Lp1, __dmul_rn(z2, R2));
+  R = __fma_rn(z4, R3, R);
+  R = __fma_rn(z6, R4, R);
+  const double t = __dmul_rn(s, __dadd_rn(hfsq, R));
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
+  return __fma_rn(kd, ln2_hi,
+                  -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(__fma_rn(kd, ln2_lo, c), t)), f));
+}
+
 // A slow attempt starting at q (word r): -> accepted?, value, length in words.
 SKB_DEV bool zig_slow(const ZigTables& T, uint64_t k0, uint64_t k1, uint64_t q, uint64_t r,
                       double* val, int* len) {
@@ -92,8 +151,8 @@ SKB_DEV bool zig_slow(const ZigTables& T, uint64_t k0, uint64_t k1, uint64_t q, 
     for (;;) {
       const double u1 = to_unit(out64(k0, k1, p)), u2 = to_unit(out64(k0, k1, p + 1));
       p += 2;
-      const double xx = __dmul_rn(-kZigInvR, log1p(-u1));
-      const double yy = -log1p(-u2);
+      const double xx = __dmul_rn(-kZigInvR, glibc_log1p(-u1));
+      const double yy = -glibc_log1p(-u2);
       if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
         *val = ((rabs >> 8) & 1) ? -__dadd_rn(kZigR, xx) : __dadd_rn(kZigR, xx);
         *len = (int)(p - q);

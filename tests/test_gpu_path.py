@@ -400,31 +400,23 @@ def test_config1_lockstep_s1(P):
 
 def test_gaussian_sketch_bit_exact(P):
     """K9: W = standard_normal((n, w)) / sqrt(w) reproduced bit for bit, incl. the
-    ziggurat's wedge/tail slow paths (~0.7% of draws) and a row-block slice."""
+    ziggurat's wedge/tail slow paths (~0.7% of draws; the tail's log1p is glibc's,
+    restated in csrc/skb_gauss.cu) and a row-block slice."""
     import hashlib
     from paper_2209_08722_b200 import sketching as S
     with open(os.path.join(GOLDEN, "gaussian_traces.json")) as f:
         gold = json.load(f)
-    exact = 0
     for case in gold["sketch"]:
         W = S.build_gaussian_sketch(case["n"], case["w"], case["seed"])
         h = _h(W.dense)
-        exact += hashlib.sha256(np.ascontiguousarray(h).tobytes()).hexdigest() == case["sha256"]
+        assert hashlib.sha256(np.ascontiguousarray(h).tobytes()).hexdigest() == case["sha256"]
         ref = O.gaussian_sketch(case["n"], case["w"], case["seed"])
-        bad = np.nonzero(h != ref)
-        # The stream never desynchronises (every other draw is identical). The only
-        # differences allowed are last-ulp ones in tail draws (|z| > r = 3.654, ~0.03%
-        # of draws), whose value is r + log1p(.)/r: CUDA's log1p and glibc's differ
-        # by one ulp on ~0.4% of arguments (measured: 5 of 4,000,000 draws).
-        z = np.abs(ref[bad]) * np.sqrt(case["w"])
-        assert np.all(z > 3.6541528853610088), z
-        assert np.all(np.abs(h[bad] - ref[bad]) <= 2 * np.spacing(np.abs(ref[bad])))
-        assert len(bad[0]) <= 1e-5 * h.size + 1
-    assert exact >= 2
+        print(f"[gaussian W n={case['n']} w={case['w']}] differing draws: "
+              f"{int(np.count_nonzero(h != ref))} of {h.size}")
+        assert np.array_equal(h, ref)
     full = O.gaussian_sketch(5000, 37, 44)
     part = S.build_gaussian_sketch(5000, 37, 44, rows=(1234, 4321))
-    assert np.array_equal(_h(part.dense), full[1234:4321]) or \
-        np.max(np.abs(_h(part.dense) - full[1234:4321])) <= 1e-15
+    assert np.array_equal(_h(part.dense), full[1234:4321])
 
 
 @pytest.mark.parametrize("name,emu", [("wide", "1"), ("illcond", "1"), ("wide", "2"),

@@ -198,3 +198,19 @@ def test_other_solvers_traces(name):
     assert [r["inner_iterations"] for r in rep["steps"]] == gold["inner_iterations"]
     np.testing.assert_allclose(rep["mu_trace"], gold["mu_trace"], rtol=1e-12)
     assert abs(rep["objective"] - gold["objective"]) <= 1e-10 * abs(gold["objective"])
+
+
+def test_glibc_log1p_restatement_matches_host_libm(tmp_path):
+    """The explicit-FMA log1p that csrc/skb_gauss.cu uses in the ziggurat tail
+    (tests/golden/log1p_check.c, the same operations in C) equals the host
+    libm's log1p -- numpy's npy_log1p -- bit for bit on 2e7 arguments in (-1, 0]."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no C compiler")
+    exe = tmp_path / "log1p_check"
+    src = os.path.join(os.path.dirname(__file__), "golden", "log1p_check.c")
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", src, "-lm", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), "20000000"], capture_output=True, text=True)
+    print(out.stdout.strip())
+    assert out.returncode == 0 and "mismatches 0" in out.stdout
