@@ -104,6 +104,15 @@ int skb_directions(const double* A, int64_t m, int64_t n, int64_t lda, const dou
                    double sigma_mu, double* ds, double* dx, double* atdy, double* adx,
                    void* workspace, size_t ws_bytes, void* stream);
 
+/* skb_directions plus avs = A (v ./ s), the v-invariant recheck's product
+ * (ipm_core.py:502), in the same pass over A; adx and avs are bitwise those of
+ * skb_directions and skb_gemv_ratio. Dense m <= 1024 only (else
+ * SKB_ERR_UNSUPPORTED: use the two separate passes). */
+int skb_directions_v(const double* A, int64_t m, int64_t n, int64_t lda, const double* dy,
+                     const double* x, const double* s, const double* v, const double* r_d,
+                     double sigma_mu, double* ds, double* dx, double* atdy, double* adx,
+                     double* avs, void* workspace, size_t ws_bytes, void* stream);
+
 /* One pass of make_iterate (ipm_core.py:94-102) at x + alpha dx, y_new, s + alpha ds:
  * x_out, s_out (nullable), r_d = A' y_new + s_new - c, r_p = A x_new - b.
  * dx/ds may be NULL (alpha ignored). */

@@ -18,6 +18,7 @@
 // result is deterministic run to run.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cub/block/block_radix_sort.cuh>
 
@@ -168,6 +169,29 @@ struct OpIter {  // make_iterate at x + a dx, y_new (=z), s + a ds (ipm_core.py:
   }
 };
 
+// assemble_directions plus the v-invariant recheck's A (v ./ s) in the same
+// pass (ipm_core.py:218-223 and :502): a second accumulator with coefficient
+// v_j / s_j. Per lane and column the two accumulations are exactly those of
+// OpDir and OpGemvRatio, so adx and A (v ./ s) are bitwise the separate passes'.
+struct OpDirV : OpDir {
+  static constexpr bool kAxpy2 = true;
+  SKB_DEV double coef2(const Pre& p) const { return ddiv(p.v[2], p.v[1]); }
+};
+
+template <class Op, class = void>
+struct Axpy2 {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct Axpy2<Op, std::void_t<decltype(Op::kAxpy2)>> {
+  static constexpr bool value = Op::kAxpy2;
+};
+template <class Op>
+SKB_DEV double coef2_of(const Op& op, const Pre& p) {
+  if constexpr (Axpy2<Op>::value) return op.coef2(p);
+  else return 0.0;
+}
+
 // --------------------------------------------------------------- kernel
 
 template <int R2, bool ZREG, class Op>
@@ -195,8 +219,10 @@ __global__ void __launch_bounds__(256, 1)
   }
   __syncthreads();
 
+  constexpr bool A2 = Axpy2<Op>::value;
   double zr[ZREG ? 2 * R2 : 1];
   double acc[Op::kAxpy ? 2 * R2 : 1];
+  double acc2[A2 ? 2 * R2 : 1];
 #pragma unroll
   for (int k = 0; k < R2; ++k) {
 #pragma unroll
@@ -204,6 +230,7 @@ __global__ void __launch_bounds__(256, 1)
       const int r = 64 * k + 2 * lane + e;
       if (ZREG && Op::kDot) zr[2 * k + e] = r < m ? z[r] : 0.0;
       if (Op::kAxpy) acc[2 * k + e] = 0.0;
+      if (A2) acc2[2 * k + e] = 0.0;
     }
   }
 
@@ -235,11 +262,12 @@ __global__ void __launch_bounds__(256, 1)
     for (int c = 0; c < cnt; ++c) {
       const double* col = buf + (size_t)c * lda;
       if constexpr (!ZREG) {
-        // large m: stream the column from shared memory twice (dot, then axpy)
+        // stream the column from shared memory twice (dot, then axpy), z from
+        // shared memory: frees the registers for a second accumulator (OpDirV)
         double dot = 0.0;
         if (Op::kDot) {
           double d0 = 0.0, d1 = 0.0;
-#pragma unroll 8
+#pragma unroll
           for (int k = 0; k < R2; ++k) {
             const int r = 64 * k + 2 * lane;
             if (r < m) {
@@ -254,6 +282,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int q = 0; q < Op::kPre; ++q) pc.v[q] = __shfl_sync(0xffffffffu, pre.v[q], c);
         const double cf = op.coef(c0 + c, pc, dot);
+        const double cf2 = coef2_of(op, pc);
         if (lane == 0) op.emit(c0 + c, pc, dot, cf);
         if (Op::kAxpy) {
 #pragma unroll
@@ -266,6 +295,10 @@ __global__ void __launch_bounds__(256, 1)
             }
             acc[2 * k] = fma(cf, t.x, acc[2 * k]);
             acc[2 * k + 1] = fma(cf, t.y, acc[2 * k + 1]);
+            if constexpr (A2) {
+              acc2[2 * k] = fma(cf2, t.x, acc2[2 * k]);
+              acc2[2 * k + 1] = fma(cf2, t.y, acc2[2 * k + 1]);
+            }
           }
         }
         continue;
@@ -327,6 +360,24 @@ __global__ void __launch_bounds__(256, 1)
     double s = 0.0;
     for (int w = 0; w < nw; ++w) s += red[(size_t)w * m + r];
     part[(size_t)blockIdx.x * m + r] = s;
+  }
+  if constexpr (A2) {  // second m-vector: partials after the first block of partials
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < R2; ++k) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 64 * k + 2 * lane + e;
+        if (r < m) red[(size_t)warp * m + r] = acc2[2 * k + e];
+      }
+    }
+    __syncthreads();
+    double* part2 = part + (size_t)gridDim.x * m;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += red[(size_t)w * m + r];
+      part2[(size_t)blockIdx.x * m + r] = s;
+    }
   }
 }
 
@@ -865,6 +916,43 @@ extern "C" int skb_directions(const double* A, int64_t m, int64_t n, int64_t lda
   SKB_WS;
   OpDir op{x, s, v, r_d, sigma_mu, ds, dx, atdy};
   return run_stream(A, lda, (int)m, n, dy, adx, nullptr, op, &ws, (cudaStream_t)stream);
+}
+
+extern "C" int skb_directions_v(const double* A, int64_t m, int64_t n, int64_t lda,
+                                const double* dy, const double* x, const double* s,
+                                const double* v, const double* r_d, double sigma_mu, double* ds,
+                                double* dx, double* atdy, double* adx, double* avs,
+                                void* workspace, size_t ws_bytes, void* stream) {
+  // dense column-stream path only (m <= 1024): z from shared memory, which
+  // leaves the registers for the second accumulator
+  if (m < 1 || m > 1024 || n < 1 || lda < m || (lda & 1) || ((uintptr_t)A & 15))
+    return SKB_ERR_UNSUPPORTED;
+  SKB_WS;
+  cudaStream_t st = (cudaStream_t)stream;
+  OpDirV op;
+  static_cast<OpDir&>(op) = OpDir{x, s, v, r_d, sigma_mu, ds, dx, atdy};
+  const StreamCfg c = stream_cfg((int)m, n, lda);
+  double* part = (double*)skb_ws_take(&ws, (size_t)2 * c.grid * m * 8);
+  if (!part) return SKB_ERR_WORKSPACE;
+  int rc;
+  // (z in registers too spills at m = 1000: 2.71 ms against 1.68 ms from shared memory;
+  // the two separate passes take 2.45 ms)
+  if (m <= 64)
+    rc = launch_r2<1, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
+  else if (m <= 128)
+    rc = launch_r2<2, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
+  else if (m <= 256)
+    rc = launch_r2<4, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
+  else if (m <= 512)
+    rc = launch_r2<8, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
+  else
+    rc = launch_r2<16, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
+  if (rc) return rc;
+  reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(part, c.grid, (int)m, nullptr,
+                                                                    adx, nullptr);
+  reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(
+      part + (size_t)c.grid * m, c.grid, (int)m, nullptr, avs, nullptr);
+  return skb_launch_status(__func__);
 }
 
 extern "C" int skb_iterate(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,

@@ -133,21 +133,27 @@ class SparseDeviceMatrix:
                 self._ell = buf
         return self._ell
 
+    DET_MAX_NNZ = 1 << 24
+
     def plan(self, force: bool = False):
-        """Build (once) the pass plan of the deterministic CSC passes: on
-        request, or for every matrix when SKB_CSC_PLAN=1. At c4 the planned
-        pass is bitwise reproducible but slower than the atomic one (0.69 vs
-        0.47 ms), so it is opt-in."""
+        """Build (once) the pass plan of the deterministic CSC passes. Default:
+        for matrices up to DET_MAX_NNZ nonzeros, whose passes are launch-bound
+        anyway, so every CSC result there is bitwise reproducible run to run;
+        above it (c4: 1e8 nnz) the shared-atomic passes, which are faster
+        (0.47 vs 0.69 ms at c4) but sum in arbitration order.
+        SKB_CSC_PLAN=1 plans every matrix, SKB_CSC_PLAN=0 none."""
         import os
-        want = force or os.environ.get("SKB_CSC_PLAN", "0") == "1"
-        if getattr(self, "_plan", None) is None or (want and self._plan[0] is None
-                                                       and not getattr(self, "_plan_tried", False)):
+        env = os.environ.get("SKB_CSC_PLAN", "")
+        if getattr(self, "_plan", None) is None or (
+                (force or env == "1") and self._plan[0] is None
+                and not getattr(self, "_plan_tried", False)):
             self._plan = (None, 0)
+            nnz = int((self.colptr[-1] - self.colptr[0]).item()) if self.n > 0 else 0
+            want = force or env == "1" or (env != "0" and nnz <= self.DET_MAX_NNZ)
             if want and self.n > 0:
                 self._plan_tried = True
                 lens = self.colptr[1:] - self.colptr[:-1]
                 maxlen = int(lens.max().item())
-                nnz = int((self.colptr[-1] - self.colptr[0]).item())
                 nb = int(_lib.lib().skb_csc_plan_bytes(self.m, self.n, nnz, maxlen))
                 if nb > 0:
                     buf = torch.empty(nb, dtype=torch.uint8, device=self.vals.device)
@@ -228,6 +234,22 @@ def directions(A, dy, x, s, v, sigma_mu, ds, dx, adx, atdy=None, r_d=None):
     pre, args = _amat(A)
     _lib.call(pre + "directions", *args, dy, x, s, v, _p(r_d), float(sigma_mu), ds, dx, _p(atdy),
               adx, ws, cap, stream_ptr())
+
+
+def directions_v(A, dy, x, s, v, sigma_mu, ds, dx, adx, avs, atdy=None, r_d=None) -> bool:
+    """directions() plus avs = A (v / s) in the same pass (ipm_core.py:218-223, :502);
+    False where the fused pass does not apply (CSC, m > 1024): use the two passes."""
+    if isinstance(A, SparseDeviceMatrix) or A.m > 1024:
+        return False
+    ws, cap = _ws(A.m)
+    try:
+        _lib.call("skb_directions_v", A.cols, A.m, A.n, A.lda, dy, x, s, v, _p(r_d),
+                  float(sigma_mu), ds, dx, _p(atdy), adx, avs, ws, cap, stream_ptr())
+    except _lib.SkbError as e:
+        if e.code == -6:  # SKB_ERR_UNSUPPORTED: the caller runs the two passes
+            return False
+        raise
+    return True
 
 
 def iterate(A, x, s, y_new, b, c, r_p, r_d, dx=None, ds=None, alpha=0.0, x_out=None,

@@ -223,6 +223,21 @@ class DeviceLP:
         self._finish_m(adx, None)
         return dx, ds, atdy, adx
 
+    def directions_v(self, dy, x, s, v, sigma_mu, r_d=None, sub=None):
+        """directions() and A (v / s) [- sub] from one pass over A, or None where
+        the fused pass does not apply (then: directions() and gemv_ratio())."""
+        ds, dx, atdy, adx, avs = self.new_n(), self.new_n(), self.new_n(), self.new_m(), \
+            self.new_m()
+        if not K.directions_v(self.A, dy, x, s, v, sigma_mu, ds, dx, adx, avs, atdy=atdy,
+                              r_d=r_d):
+            return None
+        self._finish_m(adx, None)
+        if self.comm.active:
+            self._finish_m(avs, sub)
+        elif sub is not None:
+            _lib.call("skb_sub", avs, sub, avs, self.m, stream_ptr())
+        return (dx, ds, atdy, adx), avs
+
     def iterate(self, x, s, y_new, dx=None, ds=None, alpha=0.0):
         """-> (x_new, s_new, r_p, r_d) of make_iterate at the step."""
         xo = self.new_n() if dx is not None else x

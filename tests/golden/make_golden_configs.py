@@ -19,6 +19,8 @@ Cases (SURVEY.md §8(d) generators; gamma widened as in App. C):
   m2000     wide_dense_lp(2000, 100_000, 2),   w=8000, s=4, 6 steps (warp-pair K4)
   sparse1e4 sparse_wide_lp(10_000, 200_000, 5, 3), w=40_000, s=4, 3 steps
             (L2 CSC sketch, INT8-emulated factor GEMMs at m=1e4)
+  c4        sparse_wide_lp(10_000, 20_000_000, 5, 4) -- c4 itself, 1e8 nnz -- w=40_000, s=4,
+            2 steps (the reference's gesdd of the 1e4 x 4e4 sketch dominates its step)
   c5m1000   ill_conditioned_lp(1000, 20_000, 4), Gaussian w=4000, sigma=0.3, 6 steps
             (scipy's sparse x dense AD @ W is single-threaded: ~1 min per sketch here)
 """
@@ -56,6 +58,8 @@ CASES = {
                       sigma=0.5, tol=1e-8, steps=3, seed=3),
     "c5m1000": dict(gen=("ill", 1000, 20_000, 4), w=4000, sketch="gaussian", s=(0,),
                     sigma=0.3, tol=1e-8, steps=6, seed=4),
+    "c4": dict(gen=("sparse", 10_000, 20_000_000, 4), w=40_000, sketch="sparse", s=(4,),
+               sigma=0.5, tol=1e-8, steps=2, seed=4),
 }
 
 

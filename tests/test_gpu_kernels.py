@@ -292,3 +292,26 @@ def test_potrf_fused_steps_bitwise_equal_panel_loop(K, monkeypatch, Mp):
         st = torch.zeros(1, dtype=torch.int32, device="cuda")
         _lib.call("skb_potrf", _t(bad), Mp, Mp, st, ws, cap, stream_ptr())
         assert int(st.item()) & 4
+
+
+@pytest.mark.parametrize("m,n,mode", [(37, 3001, "feasible"), (100, 5000, "infeasible"),
+                                      (512, 20000, "feasible"), (1000, 50001, "infeasible")])
+def test_directions_v_fused_bitwise(K, m, n, mode):
+    """skb_directions_v (assemble_directions + the v-invariant's A (v / s) in one
+    pass, z from shared memory) against skb_directions and skb_gemv_ratio:
+    every output bitwise identical."""
+    g, A = _problem(m, n, m + 11)
+    x, s = g.random(n) + 0.2, g.random(n) + 0.2
+    dy, v = g.standard_normal(m), 1e-3 * g.standard_normal(n)
+    r_d = _t(1e-2 * g.standard_normal(n)) if mode == "infeasible" else None
+    Ad = K.DeviceMatrix.from_host(A)
+    e = lambda k: torch.empty(k, dtype=torch.float64, device="cuda")  # noqa: E731
+    ref = [e(n), e(n), e(m), e(n), e(m)]
+    K.directions(Ad, _t(dy), _t(x), _t(s), _t(v), 0.123, ref[0], ref[1], ref[2], atdy=ref[3],
+                 r_d=r_d)
+    K.gemv_ratio(Ad, _t(v), _t(s), ref[4])
+    out = [e(n), e(n), e(m), e(n), e(m)]
+    assert K.directions_v(Ad, _t(dy), _t(x), _t(s), _t(v), 0.123, out[0], out[1], out[2],
+                          out[4], atdy=out[3], r_d=r_d)
+    for a, b in zip(out, ref):
+        assert np.array_equal(_h(a), _h(b))
