@@ -18,6 +18,8 @@ prints the largest deviation it measured.
   m2000      2000 x 1e5 dense, w=8000, s=4: 6 steps (the warp-pair K4 kernel)
   sparse1e4  1e4 x 2e5 CSC (5 nnz/col), w=4e4, s=4: 3 steps (L2 CSC sketch,
              INT8-emulated factor GEMMs)
+  c4         c4 itself: 1e4 x 2e7 CSC (1e8 nnz), w=4e4, s=4: 2 steps (the CSC sketch
+             and the INT8-emulated factor at full size; the reference takes 436 s a step)
   c5m1000    ill-conditioned 1000 x 2e4, Gaussian w=4000, sigma=0.3: 6 steps
 """
 
@@ -31,7 +33,7 @@ pytestmark = pytest.mark.gpu
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLDEN = os.path.join(HERE, "golden")
-CASES = ["c2", "m1000", "m2000", "sparse1e4", "c5m1000"]
+CASES = ["c2", "m1000", "m2000", "sparse1e4", "c4", "c5m1000"]
 
 
 def _load(case):
