@@ -100,6 +100,17 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
   }
 }
 
+// start[b] = first position of bucket b in the sorted keys (start[w] = N): each
+// boundary i (keys[i-1] != keys[i], or the ends) fills the buckets in between.
+__global__ void bucket_starts_kernel(const uint32_t* __restrict__ keys, int64_t N, int w,
+                                     uint64_t* __restrict__ start) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > N) return;
+  const int64_t kp = i == 0 ? -1 : (int64_t)keys[i - 1];
+  const int64_t kc = i == N ? (int64_t)w : (int64_t)keys[i];
+  for (int64_t b = kp + 1; b <= kc; ++b) start[b] = (uint64_t)i;
+}
+
 __global__ void scan_buckets_kernel(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
                                     int n) {
   __shared__ uint64_t part[1024];
@@ -343,13 +354,13 @@ static int bucket_sort_radix(const int32_t* cols, const double* vals, int64_t N,
   cudaMemsetAsync(counter, 0, 16, st);
   int bits = 1;
   while ((1ll << bits) < (int64_t)w) ++bits;
-  size_t b1 = tb;
-  cub::DeviceHistogram::HistogramEven(tmp, b1, cols, total, (int)w + 1, 0, (int)w, (int)N, st);
-  scan_buckets_kernel<<<1, 1024, 0, st>>>(total, start, w);
+  (void)total;
   iota_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(iota, vals, N);
   size_t b2 = tb;
   cub::DeviceRadixSort::SortPairs(tmp, b2, reinterpret_cast<const uint32_t*>(cols), keys, iota,
                                   mem_e, (int)N, 0, bits, st);
+  // bucket starts from the sorted keys' boundaries (no separate histogram pass)
+  bucket_starts_kernel<<<(unsigned)((N + 1 + 255) / 256), 256, 0, st>>>(keys, N, w, start);
   *start_out = start;
   *mem_out = mem_e;
   *counter_out = counter;
