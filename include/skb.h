@@ -281,6 +281,17 @@ int skb_i8gemm_batched(const int8_t* A, int64_t Ra, int64_t sa, const int8_t* B,
                        int32_t cols, int32_t ar0, int32_t br0, int32_t k0, int32_t k1, int32_t n,
                        int32_t tri, int32_t tri_off, void* stream);
 
+/* skb_i8gemm_batched with a residue epilogue: each int32 product is stored as its
+ * symmetric residue mod mod[l] in int8 (C8: row stride ldc8, batch stride sc8, in
+ * bytes, multiples of 16; p = 256 ties as -128), which is all the FP64
+ * emulation's CRT needs (preconditioning.py:46 / sketching.py:158-159 products).
+ * Persistent 2-SM kernel; n <= 24. */
+int skb_i8gemm_residues(const int8_t* A, int64_t Ra, int64_t sa, const int8_t* B, int64_t Rb,
+                        int64_t sb, int64_t Kp, int8_t* C8, int64_t ldc8, int64_t sc8,
+                        int32_t rows, int32_t cols, int32_t ar0, int32_t br0, int32_t k0,
+                        int32_t k1, int32_t n, int32_t tri, int32_t tri_off, const double* mod,
+                        void* stream);
+
 /* One-shot all-reduce of an m-vector over NVLink peer memory (csrc/skb_p2p.cu):
  * the exchange SURVEY.md §8(e) puts after every sharded A-pass that yields an
  * m-vector (reference: the single-process sums of krylov_solvers.py:46-47,

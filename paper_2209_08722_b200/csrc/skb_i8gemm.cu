@@ -392,12 +392,21 @@ struct PCfg {
   static constexpr int NACC = NB == 1 ? 2 : 1;          // TMEM accumulators
 };
 
+// Residue epilogue (res.on): instead of the int32 products, store their symmetric
+// residues mod p_z as int8 (r = c - rint(c / p) p, exact: |c| < 2^31, and a
+// non-tie quotient is >= 0.5/p from a half-integer; p = 256 ties store -128),
+// so the CRT reads 1 byte per product instead of 4 (skb_ozaki.cu).
+struct ResMod {
+  int on;
+  double p[24], pinv[24];
+};
+
 template <int NB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q_THREADS, 1)
     i8gemm2p_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                     int32_t* __restrict__ C, int64_t ldc, int64_t mstride, int rows, int cols,
                     int arow0, int brow0, int kb0, int nkb, int TM, int TN, int nz, int tri,
-                    int tri_off) {
+                    int tri_off, const __grid_constant__ ResMod res) {
   using Cfg = PCfg<NB>;
   extern __shared__ uint8_t smraw[];
   __shared__ __align__(8) uint64_t full[Cfg::NST], empty[Cfg::NST], tfull[2], tempty[2];
@@ -526,7 +535,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q_THREADS, 1)
       mbar_wait(&tfull[b], (uint32_t)(use & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = tm * P_BM + (int)rank * 128 + warp * 32 + lane;
-      int32_t* crow = C + (int64_t)z * mstride + (int64_t)row * ldc + (int64_t)tn * Cfg::BN;
+      int32_t* crow = res.on ? C
+                             : C + (int64_t)z * mstride + (int64_t)row * ldc + (int64_t)tn * Cfg::BN;
       const int cmax = cols - tn * Cfg::BN;
 #pragma unroll 1
       for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
@@ -545,12 +555,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q_THREADS, 1)
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row < rows) {
+          if (res.on) {  // int8 residues: C is a byte slab (ldc, mstride in bytes)
+            const double pz = res.p[z], piz = res.pinv[z];
+            constexpr double kMg = 6755399441055744.0;  // 1.5 * 2^52
+            uint32_t w[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (c0 + 4 * q < cmax)
-              *reinterpret_cast<int4*>(crow + c0 + 4 * q) =
-                  make_int4((int)v[4 * q], (int)v[4 * q + 1], (int)v[4 * q + 2],
-                            (int)v[4 * q + 3]);
+            for (int q = 0; q < 8; ++q) {
+              uint32_t bytes[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const double dd = (double)(int)v[4 * q + u];
+                const double qq = fma(dd, piz, kMg) - kMg;
+                bytes[u] = (uint32_t)__double2loint(fma(-qq, pz, dd) + kMg);
+              }
+              w[q] = __byte_perm(__byte_perm(bytes[0], bytes[1], 0x0040),
+                                 __byte_perm(bytes[2], bytes[3], 0x0040), 0x5410);
+            }
+            int8_t* c8 = reinterpret_cast<int8_t*>(C) + (int64_t)z * mstride +
+                         (int64_t)row * ldc + (int64_t)tn * Cfg::BN + c0;
+            if (c0 < cmax) *reinterpret_cast<uint4*>(c8) = make_uint4(w[0], w[1], w[2], w[3]);
+            if (c0 + 16 < cmax)
+              *reinterpret_cast<uint4*>(c8 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (c0 + 4 * q < cmax)
+                *reinterpret_cast<int4*>(crow + c0 + 4 * q) =
+                    make_int4((int)v[4 * q], (int)v[4 * q + 1], (int)v[4 * q + 2],
+                              (int)v[4 * q + 3]);
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -620,15 +653,15 @@ using namespace skb;
 // cols % 16 == 0. tri = 1: only the tiles meeting the lower triangle col <= row
 // + tri_off are computed (the others are left untouched; persistent 2-SM path).
 // Returns 0, or SKB_ERR_* (no CPU or library fallback).
-extern "C" int skb_i8gemm_batched(const int8_t* A, int64_t Ra, int64_t sa, const int8_t* B,
-                                  int64_t Rb, int64_t sb, int64_t Kp, int32_t* C, int64_t ldc,
-                                  int64_t sc, int32_t rows, int32_t cols, int32_t ar0,
-                                  int32_t br0, int32_t k0, int32_t k1, int32_t n, int32_t tri,
-                                  int32_t tri_off, void* stream) {
+static int i8gemm_run(const int8_t* A, int64_t Ra, int64_t sa, const int8_t* B, int64_t Rb,
+                      int64_t sb, int64_t Kp, int32_t* C, int64_t ldc, int64_t sc, int32_t rows,
+                      int32_t cols, int32_t ar0, int32_t br0, int32_t k0, int32_t k1, int32_t n,
+                      int32_t tri, int32_t tri_off, const skb::i8::ResMod& res, void* stream) {
   using namespace skb::i8;
   if (rows <= 0 || cols <= 0 || n <= 0) return 0;
   if (k1 <= k0 || (k0 % BK) || (cols % 16) || (Kp % 16) || ((uintptr_t)A & 15) ||
-      ((uintptr_t)B & 15) || (ldc % 4) || (sc % 4) || ((uintptr_t)C & 15))
+      ((uintptr_t)B & 15) || (ldc % (res.on ? 16 : 4)) || (sc % (res.on ? 16 : 4)) ||
+      ((uintptr_t)C & 15) || (res.on && n > 24))
     return SKB_ERR_ARG;
   CUtensorMap ma, mb;
   static const bool one_sm0 = getenv("SKB_I8_1SM") && getenv("SKB_I8_1SM")[0] == '1';
@@ -646,11 +679,11 @@ extern "C" int skb_i8gemm_batched(const int8_t* A, int64_t Ra, int64_t sa, const
   }
   const int nkb = (k1 - k0 + BK - 1) / BK;
   static const bool one_sm = getenv("SKB_I8_1SM") && getenv("SKB_I8_1SM")[0] == '1';
-  if (one_sm) {
+  if (!res.on && one_sm) {
     dim3 grid((unsigned)((cols + BN - 1) / BN), (unsigned)((rows + BM - 1) / BM), (unsigned)n);
     i8gemm_kernel<<<grid, 128, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, C, ldc, sc, rows,
                                                                    cols, ar0, br0, k0, nkb);
-  } else if (getenv("SKB_I8_NP") && getenv("SKB_I8_NP")[0] == '1') {  // non-persistent pairs
+  } else if (!res.on && getenv("SKB_I8_NP") && getenv("SKB_I8_NP")[0] == '1') {  // non-persistent
     dim3 grid((unsigned)(2 * ((cols + P_BN - 1) / P_BN)), (unsigned)((rows + P_BM - 1) / P_BM),
               (unsigned)n);
     i8gemm2_kernel<<<grid, 128, P_SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, C, ldc, sc, rows,
@@ -679,10 +712,42 @@ extern "C" int skb_i8gemm_batched(const int8_t* A, int64_t Ra, int64_t sa, const
     const int pairs = std::max(1, std::min(skb_num_sms() / 2, per_z * n));
     if (wide)
       i8gemm2p_kernel<2><<<2 * pairs, Q_THREADS, PCfg<2>::SMEM, (cudaStream_t)stream>>>(
-          ma, mb, C, ldc, sc, rows, cols, ar0, br0, k0, nkb, TM, TN, n, tri ? 1 : 0, tri_off);
+          ma, mb, C, ldc, sc, rows, cols, ar0, br0, k0, nkb, TM, TN, n, tri ? 1 : 0, tri_off,
+          res);
     else
       i8gemm2p_kernel<1><<<2 * pairs, Q_THREADS, PCfg<1>::SMEM, (cudaStream_t)stream>>>(
-          ma, mb, C, ldc, sc, rows, cols, ar0, br0, k0, nkb, TM, TN, n, tri ? 1 : 0, tri_off);
+          ma, mb, C, ldc, sc, rows, cols, ar0, br0, k0, nkb, TM, TN, n, tri ? 1 : 0, tri_off,
+          res);
   }
-  return skb_launch_status(__func__);
+  return skb_launch_status("skb_i8gemm");
+}
+
+extern "C" int skb_i8gemm_batched(const int8_t* A, int64_t Ra, int64_t sa, const int8_t* B,
+                                  int64_t Rb, int64_t sb, int64_t Kp, int32_t* C, int64_t ldc,
+                                  int64_t sc, int32_t rows, int32_t cols, int32_t ar0,
+                                  int32_t br0, int32_t k0, int32_t k1, int32_t n, int32_t tri,
+                                  int32_t tri_off, void* stream) {
+  skb::i8::ResMod res{};
+  return i8gemm_run(A, Ra, sa, B, Rb, sb, Kp, C, ldc, sc, rows, cols, ar0, br0, k0, k1, n, tri,
+                    tri_off, res, stream);
+}
+
+// As skb_i8gemm_batched, but each product is stored as its symmetric residue mod
+// mod[l] (int8 slab C8: row stride ldc8 and batch stride sc8 in bytes, multiples
+// of 16): the FP64 emulation's CRT then reads one byte per product. Persistent
+// 2-SM kernel only; n <= 24.
+extern "C" int skb_i8gemm_residues(const int8_t* A, int64_t Ra, int64_t sa, const int8_t* B,
+                                   int64_t Rb, int64_t sb, int64_t Kp, int8_t* C8, int64_t ldc8,
+                                   int64_t sc8, int32_t rows, int32_t cols, int32_t ar0,
+                                   int32_t br0, int32_t k0, int32_t k1, int32_t n, int32_t tri,
+                                   int32_t tri_off, const double* mod, void* stream) {
+  if (n > 24) return SKB_ERR_ARG;
+  skb::i8::ResMod res{};
+  res.on = 1;
+  for (int l = 0; l < n; ++l) {
+    res.p[l] = mod[l];
+    res.pinv[l] = 1.0 / mod[l];
+  }
+  return i8gemm_run(A, Ra, sa, B, Rb, sb, Kp, reinterpret_cast<int32_t*>(C8), ldc8, sc8, rows,
+                    cols, ar0, br0, k0, k1, n, tri, tri_off, res, stream);
 }

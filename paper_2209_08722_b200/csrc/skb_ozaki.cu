@@ -288,6 +288,50 @@ __global__ void __launch_bounds__(256) crt_kernel(const int32_t* __restrict__ c3
   *cp = beta == 0.0 ? alpha * val : fma(alpha, val, beta * *cp);
 }
 
+// As crt_kernel, from the int8 residues the INT8 kernel's residue epilogue
+// stored (skb_i8gemm_residues): one byte per product instead of four, the
+// per-modulus reduction already done.
+template <int NM>
+__global__ void __launch_bounds__(256) crt8_kernel(const int8_t* __restrict__ r8, int64_t ldr,
+                                                   int64_t mstride, int r0, int rows, int c0,
+                                                   int cols, int lower_only, const Table tab,
+                                                   const double* __restrict__ invA,
+                                                   const double* __restrict__ invB,
+                                                   double alpha, double beta,
+                                                   double* __restrict__ C, int64_t ldc) {
+  const int jj = blockIdx.x * 128 + (threadIdx.x & 127);
+  const int ii = blockIdx.y * 2 + (threadIdx.x >> 7);
+  if (ii >= rows || jj >= cols) return;
+  const int i = r0 + ii, j = c0 + jj;
+  if (lower_only && j > i) return;
+  const int8_t* src = r8 + (int64_t)ii * ldr + jj;
+  int rr[NM];
+#pragma unroll
+  for (int l = 0; l < NM; ++l) {  // all loads in flight
+    rr[l] = __ldg(src);
+    src += mstride;
+  }
+  double q = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+  for (int l = 0; l < NM; ++l) {
+    const double r = (double)rr[l];
+    q = fma(r, tab.yp[l], q);
+    t1 = fma(r, tab.w1[l], t1);
+    t2 = fma(r, tab.w2[l], t2);
+    t3 = fma(r, tab.w3[l], t3);
+  }
+  q = rint(q);
+  t1 = fma(-q, tab.w1[NM], t1);
+  t2 = fma(-q, tab.w2[NM], t2);
+  t3 = fma(-q, tab.w3[NM], t3);
+  const double v = fma(t1, 1099511627776.0, t2) + t3;  // 2^40
+  const double ia = __ldg(&invA[i]), ib = __ldg(&invB[j]);
+  double val = (v * (ia * tab.p2s2)) * ib;
+  if (ia == 0.0 || ib == 0.0) val = 0.0;
+  double* cp = C + (int64_t)i * ldc + j;
+  *cp = beta == 0.0 ? alpha * val : fma(alpha, val, beta * *cp);
+}
+
 // Launch K<NM> for the table's modulus count (12..20).
 #define SKB_OZ_DISPATCH(n, KERNEL, GRID, ARGS)                                          \
   switch (n) {                                                                          \
@@ -447,9 +491,13 @@ static int chunk(const skb_oz_args& g, int k0, int Kc, double beta, skb_ws* ws, 
     ws->off = mark;
     return 1;
   }
-  // INT32 tile buffer: shrink the tile height (then width) to the workspace left
+  // residue mode (default with the tcgen05 kernel): the INT8 GEMM stores int8
+  // residues, the CRT reads 1 byte per product (SKB_OZ_CRT32=1: int32 products)
+  const char* c32e = getenv("SKB_OZ_CRT32");
+  const bool r8mode = !use_cublaslt() && !(c32e && c32e[0] == '1');
+  // product tile buffer: shrink the tile height (then width) to the workspace left
   const size_t left = ws->cap > ws->off + 1024 ? ws->cap - ws->off - 1024 : 0;
-  const size_t per_elem = (size_t)n * 4;
+  const size_t per_elem = (size_t)n * (r8mode ? 1 : 4);
   if ((size_t)h * up(wc, kPadR) * per_elem > left) {
     h = (int)std::min<int64_t>(h, (int64_t)(left / (per_elem * up(wc, kPadR))) / 256 * 256);
     if (h < 128) {
@@ -463,6 +511,7 @@ static int chunk(const skb_oz_args& g, int k0, int Kc, double beta, skb_ws* ws, 
   }
   const int64_t ldt = up(wc, kPadR), mstr = (int64_t)h * ldt;
   auto* c32 = (int32_t*)skb_ws_take(ws, (size_t)mstr * per_elem);
+  auto* c8 = reinterpret_cast<int8_t*>(c32);
   if (!c32) {
     ws->off = mark;
     return 1;
@@ -517,18 +566,28 @@ static int chunk(const skb_oz_args& g, int k0, int Kc, double beta, skb_ws* ws, 
         } else {
           // the tcgen05 kernel (skb_i8gemm.cu); its K range starts on a 128-byte box:
           // entries in [kb128, kb) of these rows are outside the operand's triangle, zero
-          rc = skb_i8gemm_batched(a8, Mp, (int64_t)Mp * Kp, b8, Np, (int64_t)Np * Kp, Kp, c32,
-                                  ldt, mstr, rows_p, cols_p, r0, c0, kb / 128 * 128, ke, n,
-                                  g.lower_only ? 1 : 0, r0 - c0, st);
+          if (r8mode)
+            rc = skb_i8gemm_residues(a8, Mp, (int64_t)Mp * Kp, b8, Np, (int64_t)Np * Kp, Kp, c8,
+                                     ldt, mstr, rows_p, cols_p, r0, c0, kb / 128 * 128, ke, n,
+                                     g.lower_only ? 1 : 0, r0 - c0, tab.p, st);
+          else
+            rc = skb_i8gemm_batched(a8, Mp, (int64_t)Mp * Kp, b8, Np, (int64_t)Np * Kp, Kp,
+                                    c32, ldt, mstr, rows_p, cols_p, r0, c0, kb / 128 * 128, ke,
+                                    n, g.lower_only ? 1 : 0, r0 - c0, st);
         }
       } else {
         cudaMemsetAsync(c32, 0, (size_t)mstr * per_elem, st);
       }
       if (rc) break;
       dim3 gc((unsigned)((cols + 127) / 128), (unsigned)((rows + 1) / 2));
-      SKB_OZ_DISPATCH(n, crt_kernel, gc,
-                      (c32, ldt, mstr, r0, rows, c0, cols, g.lower_only, tab, invA, invB,
-                       g.alpha, beta, g.C, g.ldc))
+      if (r8mode)
+        SKB_OZ_DISPATCH(n, crt8_kernel, gc,
+                        (c8, ldt, mstr, r0, rows, c0, cols, g.lower_only, tab, invA, invB,
+                         g.alpha, beta, g.C, g.ldc))
+      else
+        SKB_OZ_DISPATCH(n, crt_kernel, gc,
+                        (c32, ldt, mstr, r0, rows, c0, cols, g.lower_only, tab, invA, invB,
+                         g.alpha, beta, g.C, g.ldc))
       rc = skb_launch_status("ozaki crt");
     }
   }
