@@ -582,15 +582,67 @@ SKB_DEV void tile_store_acc(double* s, const double (&acc)[4][2][2]) {
           make_double2(acc[a][b][0], acc[a][b][1]);
 }
 
+// mode 0: the fused step above. Steps with more lower tile pairs than the GPU
+// has SMs run it as two launches instead (the pair CTAs otherwise recompute
+// both panel tiles, 3 GEMMs each, over several waves): mode 1, one CTA per
+// tile row i, L_ik = A_ik Dinv_k' straight into Lo; mode 2, one CTA per pair,
+// A_ij -= L_ik L_jk' from Lo (+ the next diagonal factor). Same products in the
+// same order: bitwise identical.
 __global__ void __launch_bounds__(kLeafThreads) potrf_step_kernel(double* G, int64_t ld,
                                                                    double* Lo, int64_t ldo, int k,
-                                                                   double* Dbuf, int* status) {
+                                                                   double* Dbuf, int* status,
+                                                                   int mode) {
   extern __shared__ __align__(16) double psm[];
   double* sAi = psm;
   double* sAj = sAi + NB * kSLD;
   double* sD = sAj + NB * kSLD;
   int i = 0, j = 0;
-  if (k >= 0) {
+  if (mode == 1) {  // panel: tile row i = k + 1 + blockIdx.x
+    i = k + 1 + blockIdx.x;
+    tile_load(sAi, G + (int64_t)i * NB * ld + (int64_t)k * NB, ld);
+    tile_load(sD, Dbuf + (k & 1) * NB * NB, NB);
+    __syncthreads();
+    double acc[4][2][2];
+    tile_mm_nt(sAi, sD, acc);
+    __syncthreads();
+    tile_store_acc(sAi, acc);
+    __syncthreads();
+    double* o = Lo + (int64_t)i * NB * ldo + (int64_t)k * NB;
+    for (int e = threadIdx.x; e < NB * NB / 2; e += kLeafThreads) {
+      const int r = e >> 5, c = (e & 31) * 2;
+      *reinterpret_cast<double2*>(o + (int64_t)r * ldo + c) =
+          *reinterpret_cast<const double2*>(sAi + r * kSLD + c);
+    }
+    return;
+  }
+  if (k >= 0 && mode == 2) {
+    const int p = blockIdx.x;
+    int ii = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
+    while ((ii + 1) * (ii + 2) / 2 <= p) ++ii;
+    while (ii * (ii + 1) / 2 > p) --ii;
+    i = k + 1 + ii;
+    j = k + 1 + (p - ii * (ii + 1) / 2);
+    tile_load(sAi, Lo + (int64_t)i * NB * ldo + (int64_t)k * NB, ldo);
+    if (j != i) tile_load(sAj, Lo + (int64_t)j * NB * ldo + (int64_t)k * NB, ldo);
+    __syncthreads();
+    double acc[4][2][2];
+    tile_mm_nt(sAi, j != i ? sAj : sAi, acc);  // L_ik L_jk'
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wr = warp >> 2, wc = warp & 3, gq = lane >> 2, tq = lane & 3;
+    double* C = G + (int64_t)i * NB * ld + (int64_t)j * NB;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = wr * 32 + a * 8 + gq, c = wc * 16 + b * 8 + tq * 2 + q;
+          if (i != j || c <= r) {
+            double* dst = C + (int64_t)r * ld + c;
+            *dst = fma(1.0, *dst, -acc[a][b][q]);
+          }
+        }
+  } else if (k >= 0) {
     const int p = blockIdx.x;
     int ii = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
     while ((ii + 1) * (ii + 2) / 2 <= p) ++ii;
@@ -1025,11 +1077,19 @@ static int potrf_fused(double* G, int64_t ld, int Mp, int* status, skb_ws* ws, c
     configured = true;
   }
   const int T = Mp / NB;
-  potrf_step_kernel<<<1, kLeafThreads, kStepSmem, st>>>(G, ld, Lo, Mp, -1, Dbuf, status);
+  potrf_step_kernel<<<1, kLeafThreads, kStepSmem, st>>>(G, ld, Lo, Mp, -1, Dbuf, status, 0);
+  const char* se = getenv("SKB_POTRF_SPLIT");  // pairs above which a step is split (dev)
+  const int split_above = se ? atoi(se) : skb_num_sms();
   for (int k = 0; k + 1 < T; ++k) {
-    const int tp = T - 1 - k;
-    potrf_step_kernel<<<tp * (tp + 1) / 2, kLeafThreads, kStepSmem, st>>>(G, ld, Lo, Mp, k, Dbuf,
-                                                                          status);
+    const int tp = T - 1 - k, pairs = tp * (tp + 1) / 2;
+    if (split_above <= 0 || pairs <= split_above) {
+      potrf_step_kernel<<<pairs, kLeafThreads, kStepSmem, st>>>(G, ld, Lo, Mp, k, Dbuf, status,
+                                                                0);
+    } else {
+      potrf_step_kernel<<<tp, kLeafThreads, kStepSmem, st>>>(G, ld, Lo, Mp, k, Dbuf, status, 1);
+      potrf_step_kernel<<<pairs, kLeafThreads, kStepSmem, st>>>(G, ld, Lo, Mp, k, Dbuf, status,
+                                                                2);
+    }
   }
   const int64_t half = (int64_t)Mp * Mp / 2;
   copy_lower_tiles_kernel<<<(unsigned)((half + 255) / 256), 256, 0, st>>>(G, ld, Lo, Mp, Mp);
