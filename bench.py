@@ -545,6 +545,24 @@ def run_ours(args):
         except Exception as e:  # report, do not hide
             cpu = {"error": f"{type(e).__name__}: {e}"[:300]}
 
+    # ---- the other BASELINE configs on this GPU (kernel-level, synthetic data in HBM)
+    other = None
+    if world == 1 and args.config == "c2" and not args.no_other:
+        other = {}
+        try:
+            del dlp
+        except Exception:
+            pass
+        torch.cuda.empty_cache()
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_configs as BC
+        for name in ("c3", "c4", "c5"):
+            try:
+                other[name] = getattr(BC, name)(1.0)
+            except Exception as e:  # report, do not hide
+                other[name] = {"error": f"{type(e).__name__}: {e}"[:200]}
+            torch.cuda.empty_cache()
+
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -561,6 +579,8 @@ def run_ours(args):
             "clocks": clk.summary(),
             "sketch_precond_build": build, "ipm_solve": solve,
         }
+        if other is not None:
+            line["other_configs"] = other
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -694,6 +714,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-other", action="store_true",
+                    help="skip the c3 / c4 / c5 kernel timings of the default c2 run")
     ap.add_argument("--cpu-harness", action="store_true",
                     help="test mode: exercise the multi-rank harness over gloo without a GPU")
     args = ap.parse_args()
