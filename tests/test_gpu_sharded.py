@@ -202,3 +202,73 @@ def test_gaussian_w_stream_slices_bit_exact(world):
     full = O.gaussian_sketch(20_011, 97, 4242)
     for rank, (j0, j1), blk in res:
         assert np.array_equal(blk, full[j0:j1]), rank
+
+
+def _config_rank(rank, world, port, q, case):
+    """A config-size instance (tests/golden/cfg_<case>.json) solved column-sharded."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2209_08722_b200 import ipm_core as IC
+        from paper_2209_08722_b200.distributed import Comm
+        from paper_2209_08722_b200.errors import MaxIterations
+        from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
+        from paper_2209_08722_b200.problems import wide_dense_lp
+        with open(os.path.join(GOLDEN, f"cfg_{case}.json")) as f:
+            g = json.load(f)
+        kind, m, n, seed = g["gen"]
+        lpd = wide_dense_lp(m, n, seed)
+        dlp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c), comm=Comm())
+        prm = IC.IpmParams(mode="feasible", gamma=g["gamma_run"], sigma=g["sigma"], w=g["w"],
+                           s=4, tol_outer=g["tol_outer"], seed=g["seed"],
+                           max_outer=g["steps_limit"] or 200)
+        try:
+            rep = IC.solve(dlp, IC.make_iterate(dlp, lpd.x0, lpd.y0, lpd.s0), prm)
+        except MaxIterations as e:
+            rep = e.report
+        q.put((rank, rep.outer, [r.inner_iterations for r in rep.steps],
+               [r.sketch_seed for r in rep.steps], [r.mu_after for r in rep.steps],
+               [r.inner_residual_norms for r in rep.steps]))
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["m2000"])
+def test_sharded_config_size_vs_live_reference(case):
+    """2000 x 1e5 (warp-pair streaming kernel, w = 8000) column-sharded over 2
+    ranks (gloo, one GPU): the distributed CholeskyQR2 and the m-vector
+    all-reduces against the live reference's first 6 steps -- same seeds and
+    inner counts, mu and PCG residuals at the config gates of test_gpu_configs."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    path = os.path.join(GOLDEN, f"cfg_{case}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    import torch.multiprocessing as mp
+    with open(path) as f:
+        gold = json.load(f)["s4"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_config_rank, args=(r, 2, port, q, case)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=900) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+    assert all(r[1] != "error" for r in res), res
+    steps = gold["steps"]
+    for rank, outer, inner, seeds, mu, rn in res:
+        assert outer == gold["outer"]
+        assert inner == [s["inner_iterations"] for s in steps]
+        assert seeds == [s["sketch_seed"] for s in steps]
+        dmu = max(abs(a - s["mu_after"]) / s["mu_after"] for a, s in zip(mu, steps))
+        drn = max(float(np.max(np.abs(np.array(a) - np.array(s["inner_residual_norms"]))))
+                  / s["f_norm0"] for a, s in zip(rn, steps))
+        print(f"[sharded {case} rank {rank}] outer {outer}: mu {dmu:.2e}, residual/f0 {drn:.2e}")
+        assert dmu <= 1e-9 and drn <= 1e-9
