@@ -219,7 +219,11 @@ def _config_rank(rank, world, port, q, case):
         with open(os.path.join(GOLDEN, f"cfg_{case}.json")) as f:
             g = json.load(f)
         kind, m, n, seed = g["gen"]
-        lpd = wide_dense_lp(m, n, seed)
+        if kind == "sparse":
+            from paper_2209_08722_b200.problems import sparse_wide_lp
+            lpd = sparse_wide_lp(m, n, 5, seed)
+        else:
+            lpd = wide_dense_lp(m, n, seed)
         dlp = DeviceLP.from_host(LinearProgram(lpd.A, lpd.b, lpd.c), comm=Comm())
         prm = IC.IpmParams(mode="feasible", gamma=g["gamma_run"], sigma=g["sigma"], w=g["w"],
                            s=4, tol_outer=g["tol_outer"], seed=g["seed"],
@@ -238,12 +242,13 @@ def _config_rank(rank, world, port, q, case):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["m2000"])
+@pytest.mark.parametrize("case", ["m2000", "sparse1e4"])
 def test_sharded_config_size_vs_live_reference(case):
-    """2000 x 1e5 (warp-pair streaming kernel, w = 8000) column-sharded over 2
-    ranks (gloo, one GPU): the distributed CholeskyQR2 and the m-vector
-    all-reduces against the live reference's first 6 steps -- same seeds and
-    inner counts, mu and PCG residuals at the config gates of test_gpu_configs."""
+    """2000 x 1e5 (warp-pair streaming kernel, w = 8000) and the 1e4 x 2e5 CSC LP
+    (w = 4e4: CSC sketch, INT8-emulated Grams) column-sharded over 2 ranks (gloo,
+    one GPU): the distributed CholeskyQR2 and the m-vector all-reduces against
+    the live reference's first steps -- same seeds and inner counts, mu and PCG
+    residuals at the config gates of test_gpu_configs."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     path = os.path.join(GOLDEN, f"cfg_{case}.json")
