@@ -218,6 +218,10 @@ int skb_sketch_gather(const int32_t* cols, const double* vals, int32_t s, int64_
  * count = n*w: the whole W). Synchronises the stream.
  * skb_gaussian_apply: X = (A diag(d) W)' (w x m) as one DMMA GEMM. */
 size_t skb_gaussian_workspace_bytes(int64_t count);
+/* Extra workspace (8 bytes per stream position) that lets the generator store
+ * the fast draws' values in its classify pass instead of running Philox again
+ * in the emit pass; optional (without it: the recompute path, same bits). */
+size_t skb_gaussian_value_bytes(int64_t count);
 int skb_gaussian_sketch(uint64_t key0, uint64_t key1, int64_t lo, int64_t count, int32_t w,
                         double* W, void* workspace, size_t ws_bytes, void* stream);
 

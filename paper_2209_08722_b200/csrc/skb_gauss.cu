@@ -191,12 +191,17 @@ constexpr int kZWords = kZTile / 32;     // bitmap words per tile
 constexpr int kZListMax = 512;           // listed slow positions per tile (mean ~50)
 constexpr int kZChainWarps = 4;
 
-// ---- K9a: slow bitmap of positions [base, base + 32 * nwords)
+// ---- K9a: slow bitmap of positions [base, base + 32 * nwords). With `vals`
+// (the stored-values mode, when the workspace has room for 8 bytes per
+// position) the fast positions' final values W = x / sqrt(w) are written too,
+// at their POSITION index, and K9d only compacts them instead of running
+// Philox a second time (the slow ones are recomputed there as before).
 __global__ void __launch_bounds__(256)
     zig_classify_kernel(uint64_t k0, uint64_t k1, uint64_t base, int64_t nwords,
-                        uint32_t* __restrict__ bits) {
-  __shared__ uint64_t ki[256];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) ki[i] = zig_ki_double_bits[i];
+                        uint32_t* __restrict__ bits, double* __restrict__ vals, double sqrtw) {
+  __shared__ ZigTables T;
+  zig_load_tables(&T);
+  const double rsqrtw = __drcp_rn(sqrtw);
   __syncthreads();
   for (int64_t wd = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wd < nwords;
        wd += (int64_t)gridDim.x * blockDim.x) {
@@ -205,11 +210,17 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const u64x4 o = philox4x64_10(((p >> 2) + b) + 1, 0, 0, 0, k0, k1);
+      double v4[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint64_t r = o.v[i];
-        const uint64_t rabs = (r >> 9) & 0x000fffffffffffffULL;
-        if (!(rabs < ki[r & 0xff])) mask |= 1u << (4 * b + i);
+        if (!zig_fast(T, r)) mask |= 1u << (4 * b + i);
+        v4[i] = vals ? div_by(zig_fast_value(T, r), sqrtw, rsqrtw) : 0.0;
+      }
+      if (vals) {
+        double2* dst = reinterpret_cast<double2*>(vals + 32 * wd + 4 * b);
+        dst[0] = make_double2(v4[0], v4[1]);
+        dst[1] = make_double2(v4[2], v4[3]);
       }
     }
     bits[wd] = mask;
@@ -389,7 +400,8 @@ __global__ void __launch_bounds__(kZThreads, 3)
     zig_emit_kernel(uint64_t k0, uint64_t k1, uint64_t P0, int64_t tiles,
                     const uint32_t* __restrict__ gskip, const uint32_t* __restrict__ gacc,
                     const uint64_t* __restrict__ offs, uint64_t lo, uint64_t need,
-                    double sqrtw, double* __restrict__ out) {
+                    double sqrtw, double* __restrict__ out, const uint32_t* __restrict__ bits,
+                    const double* __restrict__ vals, uint64_t vbase) {
   __shared__ ZigTables T;
   __shared__ uint32_t warp_sum[2][kZThreads / 32];
   __shared__ double wbuf[kZThreads / 32][32 * kZPer];
@@ -408,13 +420,25 @@ __global__ void __launch_bounds__(kZThreads, 3)
     const uint32_t ac = (gacc[tile * kZWords + (tid >> 1)] >> ((tid & 1) * 16)) & 0xffffu;
     double vv[kZPer];
     uint32_t slow = 0;
+    if (vals) {  // stored-values mode: K9a's values (already / sqrt(w)) and slow bits
+      const uint64_t rel = my0 - vbase;  // a multiple of 16
+      slow = (bits[rel >> 5] >> (rel & 31)) & 0xffffu;
+      const double2* src = reinterpret_cast<const double2*>(vals + rel);
 #pragma unroll
-    for (int b = 0; b < kZPer / 4; ++b) {
-      const u64x4 o = philox4x64_10(((my0 >> 2) + b) + 1, 0, 0, 0, k0, k1);
+      for (int i = 0; i < kZPer / 2; ++i) {
+        const double2 t2 = src[i];
+        vv[2 * i] = t2.x;
+        vv[2 * i + 1] = t2.y;
+      }
+    } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        vv[4 * b + i] = zig_fast_value(T, o.v[i]);
-        if (!zig_fast(T, o.v[i])) slow |= 1u << (4 * b + i);
+      for (int b = 0; b < kZPer / 4; ++b) {
+        const u64x4 o = philox4x64_10(((my0 >> 2) + b) + 1, 0, 0, 0, k0, k1);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          vv[4 * b + i] = zig_fast_value(T, o.v[i]);
+          if (!zig_fast(T, o.v[i])) slow |= 1u << (4 * b + i);
+        }
       }
     }
     const uint32_t outm = ((~slow & 0xffffu) & ~sk) | ac;
@@ -441,7 +465,7 @@ __global__ void __launch_bounds__(kZThreads, 3)
 #pragma unroll
     for (int i = 0, k = 0; i < kZPer; ++i) {
       if (outm & (1u << i)) {
-        if (!((ac >> i) & 1u)) buf[off + k] = div_by(vv[i], sqrtw, rsqrtw);
+        if (!((ac >> i) & 1u)) buf[off + k] = vals ? vv[i] : div_by(vv[i], sqrtw, rsqrtw);
         ++k;
       }
     }
@@ -484,12 +508,17 @@ static int zig_generate(uint64_t k0, uint64_t k1, uint64_t P0, uint64_t P1, uint
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, offs, (int)(tiles + 1), st);
   void* scan_tmp = skb_ws_take(ws, scan_bytes + 16);
   if (!bits || !gskip || !gacc || !cnt || !offs || !err || !scan_tmp) return SKB_ERR_WORKSPACE;
+  // stored-values mode when the workspace has room for 8 bytes per position
+  const char* sv = getenv("SKB_ZIG_STORE");
+  double* vals = (sv && sv[0] == '0') || need <= lo
+                     ? nullptr
+                     : (double*)skb_ws_take(ws, (size_t)nwords * 32 * 8);
   if (tiles + 1 > 0x7fffffffLL) return SKB_ERR_UNSUPPORTED;
   cudaMemsetAsync(err, 0, 16, st);
   cudaMemsetAsync(cnt + tiles, 0, 8, st);
   const int sms = skb_num_sms();
   zig_classify_kernel<<<(unsigned)std::min<int64_t>((nwords + 255) / 256, 64LL * sms), 256, 0,
-                        st>>>(k0, k1, base, nwords, bits);
+                        st>>>(k0, k1, base, nwords, bits, vals, __builtin_sqrt((double)w));
   zig_chain_kernel<<<(unsigned)std::min<int64_t>((tiles + kZChainWarps - 1) / kZChainWarps,
                                                  16LL * sms),
                      32 * kZChainWarps, 0, st>>>(k0, k1, P0, base, bits, tiles, gskip, gacc, cnt,
@@ -497,7 +526,8 @@ static int zig_generate(uint64_t k0, uint64_t k1, uint64_t P0, uint64_t P1, uint
   cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, offs, (int)(tiles + 1), st);
   if (need > lo)
     zig_emit_kernel<<<(unsigned)std::min<int64_t>(tiles, 8LL * sms), kZThreads, 0, st>>>(
-        k0, k1, P0, tiles, gskip, gacc, offs, lo, need, __builtin_sqrt((double)w), out);
+        k0, k1, P0, tiles, gskip, gacc, offs, lo, need, __builtin_sqrt((double)w), out, bits,
+        vals, base);
   int herr = 0;
   skb_readback rb(st);
   rb.add(total, offs + tiles, 8);
@@ -560,6 +590,15 @@ extern "C" int skb_gaussian_range(uint64_t key0, uint64_t key1, uint64_t p0, uin
 
 // Workspace for `count` draws (or a range of ~count positions): the slow
 // bitmap, consumed / accepted bitmaps, counts, offsets and the scan scratch.
+// The stored-values mode's extra workspace (8 bytes per stream position): add it
+// to skb_gaussian_workspace_bytes when device memory allows; without it the
+// generator runs Philox twice instead.
+extern "C" size_t skb_gaussian_value_bytes(int64_t count) {
+  const uint64_t p = zig_positions_for((uint64_t)std::max<int64_t>(count, 1));
+  const uint64_t pos = p + p / 16 + (uint64_t)(kZHaloTiles + 1) * kZTile;  // one retry's growth
+  return (size_t)pos * 8 + (1u << 20);
+}
+
 extern "C" size_t skb_gaussian_workspace_bytes(int64_t count) {
   const uint64_t pos = zig_positions_for((uint64_t)std::max<int64_t>(count, 1)) * 2 +
                        (uint64_t)kZHaloTiles * kZTile;

@@ -39,7 +39,14 @@ class Workspace:
         with self._lock:
             if self._buf is None or self._buf.numel() < nbytes:
                 n = max(int(nbytes), 1 << 20)
-                n = 1 << (n - 1).bit_length()
+                if n <= 1 << 30:
+                    n = 1 << (n - 1).bit_length()   # small: powers of two
+                else:
+                    n = -(-n // (256 << 20)) * (256 << 20)  # large: 256 MB granules
+                big = self._buf is not None and self._buf.numel() >= 1 << 30
+                self._buf = None  # drop the old buffer before the new one is allocated
+                if big:
+                    torch.cuda.empty_cache()
                 self._buf = torch.empty(n, dtype=torch.uint8, device=require_cuda())
             return self._buf, self._buf.numel()
 

@@ -157,10 +157,19 @@ def build_gaussian_sketch(n: int, w: int, seed: int, rows=None, device=None,
         dense = _gaussian_rows_distributed(k0, k1, n, w, j0, j1, comm, device)
     else:
         dense = torch.empty((j1 - j0, w), dtype=F64, device=device)
-        need = int(_lib.lib().skb_gaussian_workspace_bytes(j1 * w))
+        need = _gaussian_ws_bytes(j1 * w, device)
         ws, cap = workspace(need)
         _lib.call("skb_gaussian_sketch", k0, k1, j0 * w, j1 * w, w, dense, ws, cap, stream_ptr())
     return SketchOperator(kind="gaussian", n=n, w=w, s=0, seed=int(seed), dense=dense, j0=j0)
+
+
+def _gaussian_ws_bytes(count: int, device) -> int:
+    """Generator workspace, with the stored-values scratch (8 B per stream
+    position; one Philox pass instead of two) when device memory allows it."""
+    base = int(_lib.lib().skb_gaussian_workspace_bytes(count))
+    extra = int(_lib.lib().skb_gaussian_value_bytes(count))
+    free, _ = torch.cuda.mem_get_info(device)
+    return base + extra if free > base + extra + (4 << 30) else base
 
 
 def _gaussian_rows_distributed(k0, k1, n, w, j0, j1, comm, device):
@@ -174,7 +183,7 @@ def _gaussian_rows_distributed(k0, k1, n, w, j0, j1, comm, device):
         p1 = ptot if j1 == n else (ptot * j1 // n) // ZIG_TILE * ZIG_TILE
         cap = max(1, p1 - p0)  # at most one draw per word
         buf = torch.empty(cap, dtype=F64, device=device)
-        need = int(_lib.lib().skb_gaussian_workspace_bytes(cap))
+        need = _gaussian_ws_bytes(cap, device)
         ws, wcap = workspace(need)
         cnt = np.zeros(1, dtype=np.uint64)
         _lib.call("skb_gaussian_range", k0, k1, p0, p1, w, buf, cap, cnt.ctypes.data, ws, wcap,

@@ -6,7 +6,8 @@ from paper_2209_08722_b200 import _lib
 from paper_2209_08722_b200.runtime import workspace, stream_ptr
 n, w = int(os.environ.get("PROF_N", 50_000)), 4000
 W = torch.empty((n, w), dtype=torch.float64, device="cuda")
-ws, cap = workspace(int(_lib.lib().skb_gaussian_workspace_bytes(n * w)))
+extra = int(_lib.lib().skb_gaussian_value_bytes(n * w)) if os.environ.get("SKB_ZIG_STORE", "1") != "0" else 0
+ws, cap = workspace(int(_lib.lib().skb_gaussian_workspace_bytes(n * w)) + extra)
 def gen():
     _lib.call("skb_gaussian_sketch", 123, 456, 0, n * w, w, W, ws, cap, stream_ptr())
 gen(); torch.cuda.synchronize()
