@@ -106,3 +106,31 @@ def test_first_crossing_scalar_matches_oracle():
         ref = O.first_crossing(np.array([a]), np.array([b]), np.array([c]))
         got = _first_crossing_scalar(a, b, c)
         assert (ref == got) or (math.isinf(ref) and math.isinf(got))
+
+
+def test_first_crossing_scalar_bitwise_equals_numpy_form():
+    """The plain-float _first_crossing_scalar (the step's host path) against the
+    reference's numpy expression restated for one quadratic: bitwise equal on
+    special values (+-0, +-inf, NaN, subnormals, 1e+-300) and 1e5 random cases
+    spanning 40 decades, incl. a = 0 and c slightly negative."""
+    import itertools
+    import math
+    import warnings
+    from paper_2209_08722_b200.ipm_core import _first_crossing_np, _first_crossing_scalar
+    sp_ = [0.0, -0.0, 1e-300, -1e-300, 1e300, -1e300, math.inf, -math.inf, math.nan, 1.0, -1.0,
+           1e-12, -1e-13, 5e-324]
+    g = np.random.Generator(np.random.Philox(17))
+    cases = list(itertools.product(sp_, repeat=3))
+    for _ in range(100_000):
+        a, b, c = g.standard_normal(3) * 10.0 ** g.uniform(-20, 20, 3)
+        if g.random() < 0.2:
+            a = 0.0
+        if g.random() < 0.1:
+            c = -abs(c) * 1e-14
+        cases.append((a, b, c))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for a, b, c in cases:
+            x, y = _first_crossing_scalar(a, b, c), _first_crossing_np(a, b, c)
+            assert (x == y and math.copysign(1, x) == math.copysign(1, y)) or \
+                (math.isnan(x) and math.isnan(y)), (a, b, c, x, y)

@@ -63,12 +63,14 @@ ops = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
 gaps = collections.Counter() if False else {}
 import collections as _c
 gsum = _c.Counter(); gcnt = _c.Counter()
+allgap = 0.0
 for (s0, e0, n0), (s1, e1, n1) in zip(ops, ops[1:]):
     gap = s1 - e0
+    allgap += max(gap, 0)
     if gap > 15:
         key = n0[:40] + " -> " + n1[:40]
         gsum[key] += gap; gcnt[key] += 1
 tot = sum(gsum.values())
-print(f"idle gaps > 15 us: {tot / 1e3:.2f} ms total over 4 outer")
+print(f"idle gaps > 15 us: {tot / 1e3:.2f} ms total over 4 outer; all gaps {allgap / 1e3:.2f} ms")
 for k, v in gsum.most_common(15):
     print(f"{v / 1e3:8.3f} ms  n={gcnt[k]:4d}  {k}")
