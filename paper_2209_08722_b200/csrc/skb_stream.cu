@@ -537,6 +537,7 @@ template <class Op> struct PreRing { static constexpr bool value = false; };
 template <> struct PreRing<OpDir> { static constexpr bool value = true; };
 template <> struct PreRing<OpIter> { static constexpr bool value = true; };
 template <> struct PreRing<OpRhs> { static constexpr bool value = true; };
+template <> struct PreRing<OpDirV> { static constexpr bool value = true; };
 
 template <class Op>
 SKB_DEV void prefetch_pre(const Op& op, int64_t j, double* dst) {
@@ -572,7 +573,13 @@ __global__ void __launch_bounds__(256, 1)
     fence_mbar_init();
   }
   double* mypre = pres + pair * stages * 8;
-  double zr[2 * kPairR2], acc[2 * kPairR2];
+  // two accumulators (OpDirV): z from shared memory, after the stage buffers
+  constexpr bool A2 = Axpy2<Op>::value;
+  double* zs = reinterpret_cast<double*>(
+      bufs + max((size_t)4 * stages * col_bytes, (size_t)4 * m * 8));
+  if (A2)
+    for (int r = tid; r < m; r += blockDim.x) zs[r] = z[r];
+  double zr[A2 ? 1 : 2 * kPairR2], acc[2 * kPairR2], acc2[A2 ? 2 * kPairR2 : 1];
   // warp h owns rows [h * half, min(m, (h + 1) * half)), half = ceil(m / 2) rounded to 64
   const int rbase = h * half + 2 * lane;
   const int rend = min(m, (h + 1) * half);
@@ -581,8 +588,9 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int r = rbase + 64 * k + e;
-      zr[2 * k + e] = (Op::kDot && r < rend) ? z[r] : 0.0;
+      if constexpr (!A2) zr[2 * k + e] = (Op::kDot && r < rend) ? z[r] : 0.0;
       acc[2 * k + e] = 0.0;
+      if constexpr (A2) acc2[2 * k + e] = 0.0;
     }
   }
   __syncthreads();
@@ -622,8 +630,16 @@ __global__ void __launch_bounds__(256, 1)
         const int r = rbase + 64 * k;
         if (r < rend) {
           const double2 a = *reinterpret_cast<const double2*>(col + r);
-          d0 = fma(a.x, zr[2 * k], d0);
-          d1 = fma(r + 1 < rend ? a.y : 0.0, zr[2 * k + 1], d1);
+          double z0, z1;
+          if constexpr (A2) {
+            z0 = zs[r];
+            z1 = r + 1 < rend ? zs[r + 1] : 0.0;
+          } else {
+            z0 = zr[2 * k];
+            z1 = zr[2 * k + 1];
+          }
+          d0 = fma(a.x, z0, d0);
+          d1 = fma(r + 1 < rend ? a.y : 0.0, z1, d1);
         }
       }
       const double sh = warp_sum(d0 + d1);
@@ -632,6 +648,7 @@ __global__ void __launch_bounds__(256, 1)
       dot = dots[pair * 2] + dots[pair * 2 + 1];
     }
     const double cf = op.coef(j, pre, dot);
+    const double cf2 = coef2_of(op, pre);
     if (producer) op.emit(j, pre, dot, cf);
     if (Op::kAxpy) {
 #pragma unroll
@@ -641,6 +658,10 @@ __global__ void __launch_bounds__(256, 1)
           const double2 a = *reinterpret_cast<const double2*>(col + r);
           acc[2 * k] = fma(cf, a.x, acc[2 * k]);
           acc[2 * k + 1] = fma(cf, r + 1 < rend ? a.y : 0.0, acc[2 * k + 1]);
+          if constexpr (A2) {
+            acc2[2 * k] = fma(cf2, a.x, acc2[2 * k]);
+            acc2[2 * k + 1] = fma(cf2, r + 1 < rend ? a.y : 0.0, acc2[2 * k + 1]);
+          }
         }
       }
     }
@@ -662,6 +683,22 @@ __global__ void __launch_bounds__(256, 1)
   for (int r = tid; r < m; r += blockDim.x)
     part[(size_t)blockIdx.x * m + r] =
         (red[r] + red[(size_t)m + r]) + (red[2 * (size_t)m + r] + red[3 * (size_t)m + r]);
+  if constexpr (A2) {  // second m-vector: partials after the first block of partials
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPairR2; ++k) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = rbase + 64 * k + e;
+        if (r < rend) red[(size_t)pair * m + r] = acc2[2 * k + e];
+      }
+    }
+    __syncthreads();
+    double* part2 = part + (size_t)gridDim.x * m;
+    for (int r = tid; r < m; r += blockDim.x)
+      part2[(size_t)blockIdx.x * m + r] =
+          (red[r] + red[(size_t)m + r]) + (red[2 * (size_t)m + r] + red[3 * (size_t)m + r]);
+  }
 }
 
 // out[i] = sum_b part[b][i] (fixed order: 8 interleaved slices, combined in order) - sub[i]
@@ -923,14 +960,43 @@ extern "C" int skb_directions_v(const double* A, int64_t m, int64_t n, int64_t l
                                 const double* v, const double* r_d, double sigma_mu, double* ds,
                                 double* dx, double* atdy, double* adx, double* avs,
                                 void* workspace, size_t ws_bytes, void* stream) {
-  // dense column-stream path only (m <= 1024): z from shared memory, which
-  // leaves the registers for the second accumulator
-  if (m < 1 || m > 1024 || n < 1 || lda < m || (lda & 1) || ((uintptr_t)A & 15))
+  // dense column-stream (m <= 1024) and warp-pair (1024 < m <= 2048) paths: z from
+  // shared memory, which leaves the registers for the second accumulator
+  if (m < 1 || m > 2 * kPairHalf || n < 1 || lda < m || (lda & 1) || ((uintptr_t)A & 15))
     return SKB_ERR_UNSUPPORTED;
   SKB_WS;
   cudaStream_t st = (cudaStream_t)stream;
   OpDirV op;
   static_cast<OpDir&>(op) = OpDir{x, s, v, r_d, sigma_mu, ds, dx, atdy};
+  if (m > 1024) {
+    static const bool no_pair = getenv("SKB_NO_PAIR") != nullptr;
+    if (no_pair) return SKB_ERR_UNSUPPORTED;
+    const size_t col_bytes = (size_t)lda * 8;
+    const size_t zb = (size_t)m * 8;
+    int stages = (int)std::min<size_t>(6, (218 * 1024 - 512 - kPairPreBytes - zb) /
+                                              (4 * col_bytes));
+    if (stages < 2) return SKB_ERR_UNSUPPORTED;
+    const size_t smem = 512 + kPairPreBytes +
+                        std::max((size_t)4 * stages * col_bytes, (size_t)4 * m * 8) + zb;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(skb_num_sms(), (n + 3) / 4));
+    double* part = (double*)skb_ws_take(&ws, (size_t)2 * grid * m * 8);
+    if (!part) return SKB_ERR_WORKSPACE;
+    auto kern = colpair_kernel<OpDirV>;
+    static size_t configured = 0;
+    if (smem > configured) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return SKB_ERR_CUDA;
+      configured = smem;
+    }
+    const int half = (((int)m + 1) / 2 + 63) / 64 * 64;
+    kern<<<grid, 256, smem, st>>>(A, lda, (int)m, n, stages, half, dy, part, op, nullptr);
+    reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(part, grid, (int)m,
+                                                                      nullptr, adx, nullptr);
+    reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(
+        part + (size_t)grid * m, grid, (int)m, nullptr, avs, nullptr);
+    return skb_launch_status(__func__);
+  }
   const StreamCfg c = stream_cfg((int)m, n, lda);
   double* part = (double*)skb_ws_take(&ws, (size_t)2 * c.grid * m * 8);
   if (!part) return SKB_ERR_WORKSPACE;

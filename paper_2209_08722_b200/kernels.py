@@ -238,8 +238,8 @@ def directions(A, dy, x, s, v, sigma_mu, ds, dx, adx, atdy=None, r_d=None):
 
 def directions_v(A, dy, x, s, v, sigma_mu, ds, dx, adx, avs, atdy=None, r_d=None) -> bool:
     """directions() plus avs = A (v / s) in the same pass (ipm_core.py:218-223, :502);
-    False where the fused pass does not apply (CSC, m > 1024): use the two passes."""
-    if isinstance(A, SparseDeviceMatrix) or A.m > 1024:
+    False where the fused pass does not apply (CSC, m > 2048): use the two passes."""
+    if isinstance(A, SparseDeviceMatrix) or A.m > 2048:
         return False
     ws, cap = _ws(A.m)
     try:

@@ -295,11 +295,12 @@ def test_potrf_fused_steps_bitwise_equal_panel_loop(K, monkeypatch, Mp):
 
 
 @pytest.mark.parametrize("m,n,mode", [(37, 3001, "feasible"), (100, 5000, "infeasible"),
-                                      (512, 20000, "feasible"), (1000, 50001, "infeasible")])
+                                      (512, 20000, "feasible"), (1000, 50001, "infeasible"),
+                                      (1500, 20001, "feasible"), (2000, 30000, "infeasible")])
 def test_directions_v_fused_bitwise(K, m, n, mode):
     """skb_directions_v (assemble_directions + the v-invariant's A (v / s) in one
-    pass, z from shared memory) against skb_directions and skb_gemv_ratio:
-    every output bitwise identical."""
+    pass, z from shared memory; m > 1024 through the warp-pair kernel) against
+    skb_directions and skb_gemv_ratio: every output bitwise identical."""
     g, A = _problem(m, n, m + 11)
     x, s = g.random(n) + 0.2, g.random(n) + 0.2
     dy, v = g.standard_normal(m), 1e-3 * g.standard_normal(n)

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2209_08722_b200 import kernels as K
 from paper_2209_08722_b200.runtime import F64, lda_for
-m, n = 1000, 1_000_000
+m, n = int(os.environ.get("PROF_M", 1000)), int(os.environ.get("PROF_N", 1_000_000))
 g = torch.Generator(device="cuda"); g.manual_seed(0)
 cols = torch.randn((n, lda_for(m)), dtype=F64, device="cuda", generator=g)
 A = K.DeviceMatrix(cols, m)
