@@ -272,8 +272,9 @@ __global__ void __launch_bounds__(256, 1)
             const int r = 64 * k + 2 * lane;
             if (r < m) {
               const double2 t = *reinterpret_cast<const double2*>(col + r);
-              d0 = fma(t.x, zs[r], d0);
-              if (r + 1 < m) d1 = fma(t.y, zs[r + 1], d1);
+              const double2 zz = *reinterpret_cast<const double2*>(zs + r);  // one LDS.128
+              d0 = fma(t.x, zz.x, d0);
+              if (r + 1 < m) d1 = fma(t.y, zz.y, d1);
             }
           }
           dot = warp_sum(d0 + d1);
@@ -632,8 +633,9 @@ __global__ void __launch_bounds__(256, 1)
           const double2 a = *reinterpret_cast<const double2*>(col + r);
           double z0, z1;
           if constexpr (A2) {
-            z0 = zs[r];
-            z1 = r + 1 < rend ? zs[r + 1] : 0.0;
+            const double2 zz = *reinterpret_cast<const double2*>(zs + r);  // one LDS.128
+            z0 = zz.x;
+            z1 = r + 1 < rend ? zz.y : 0.0;
           } else {
             z0 = zr[2 * k];
             z1 = zr[2 * k + 1];
