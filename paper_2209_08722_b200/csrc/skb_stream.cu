@@ -261,9 +261,8 @@ __global__ void __launch_bounds__(256, 1)
     const double* buf = reinterpret_cast<const double*>(mybuf + st * stage_bytes);
     for (int c = 0; c < cnt; ++c) {
       const double* col = buf + (size_t)c * lda;
-      if constexpr (!ZREG) {
-        // stream the column from shared memory twice (dot, then axpy), z from
-        // shared memory: frees the registers for a second accumulator (OpDirV)
+      if constexpr (!ZREG && !A2) {
+        // large m: stream the column from shared memory twice (dot, then axpy)
         double dot = 0.0;
         if (Op::kDot) {
           double d0 = 0.0, d1 = 0.0;
@@ -321,8 +320,15 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int k = 0; k < R2; ++k) {
           const int r = 64 * k + 2 * lane;
-          const double z0 = ZREG ? zr[2 * k] : (r < m ? zs[r] : 0.0);
-          const double z1 = ZREG ? zr[2 * k + 1] : (r + 1 < m ? zs[r + 1] : 0.0);
+          double z0, z1;
+          if constexpr (ZREG) {
+            z0 = zr[2 * k];
+            z1 = zr[2 * k + 1];
+          } else {  // one LDS.128 (zs has room past m: rows >= m are masked here)
+            const double2 zz = *reinterpret_cast<const double2*>(zs + r);
+            z0 = r < m ? zz.x : 0.0;
+            z1 = r + 1 < m ? zz.y : 0.0;
+          }
           d0 = fma(a[k].x, z0, d0);
           d1 = fma(a[k].y, z1, d1);
         }
@@ -334,10 +340,15 @@ __global__ void __launch_bounds__(256, 1)
       const double cf = op.coef(c0 + c, pc, dot);
       if (lane == 0) op.emit(c0 + c, pc, dot, cf);
       if (Op::kAxpy) {
+        const double cf2 = coef2_of(op, pc);  // OpDirV (z from shared memory frees the room)
 #pragma unroll
         for (int k = 0; k < R2; ++k) {
           acc[2 * k] = fma(cf, a[k].x, acc[2 * k]);
           acc[2 * k + 1] = fma(cf, a[k].y, acc[2 * k + 1]);
+          if constexpr (A2) {
+            acc2[2 * k] = fma(cf2, a[k].x, acc2[2 * k]);
+            acc2[2 * k + 1] = fma(cf2, a[k].y, acc2[2 * k + 1]);
+          }
         }
       }
     }
