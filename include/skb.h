@@ -113,6 +113,23 @@ int skb_directions_v(const double* A, int64_t m, int64_t n, int64_t lda, const d
                      double sigma_mu, double* ds, double* dx, double* atdy, double* adx,
                      double* avs, void* workspace, size_t ws_bytes, void* stream);
 
+/* make_iterate's pass at a precomputed (x_new, s_new) fused with the next step's
+ * build_rhs (ipm_core.py:94-102, :196-206): r_d = A' y_new + s_new - c,
+ * r_p = A x_new - b (b nullable), p = A (x_new - smu/s_new [- (x_new/s_new) r_d])
+ * [- r_p when p_sub_rp], smu = *smu_dev (skb_sigma_mu). r_d, r_p and p are bitwise
+ * those of skb_iterate and skb_rhs. Dense m <= 2048 (else SKB_ERR_UNSUPPORTED). */
+int skb_iterate_rhs(const double* A, int64_t m, int64_t n, int64_t lda, const double* xn,
+                    const double* sn, const double* y_new, const double* c, const double* smu_dev,
+                    int32_t infeasible, const double* b, double* r_p, double* r_d, double* p,
+                    int32_t p_sub_rp, void* workspace, size_t ws_bytes, void* stream);
+
+/* x_new = x + alpha dx, s_new = s + alpha ds (make_iterate's rounding, no FMA). */
+int skb_step_xs(const double* x, const double* dx, const double* s, const double* ds,
+                double alpha, double* xn, double* sn, int64_t n, void* stream);
+
+/* out[0] = sigma * (sum[0] / n) on the device (the next step's sigma * mu). */
+int skb_sigma_mu(const double* sum, double n, double sigma, double* out, void* stream);
+
 /* One pass of make_iterate (ipm_core.py:94-102) at x + alpha dx, y_new, s + alpha ds:
  * x_out, s_out (nullable), r_d = A' y_new + s_new - c, r_p = A x_new - b.
  * dx/ds may be NULL (alpha ignored). */

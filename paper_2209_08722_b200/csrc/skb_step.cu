@@ -276,6 +276,25 @@ __global__ void axpy_kernel(const double* __restrict__ x, double alpha,
   for (int64_t j = gtid(); j < n; j += gstride()) y[j] = x[j] + alpha * d[j];
 }
 
+// x_new = x + alpha dx, s_new = s + alpha ds with make_iterate's rounding
+// (round-to-nearest multiply then add, no FMA: skb_stream.cu OpIter).
+__global__ void step_xs_kernel(const double* __restrict__ x, const double* __restrict__ dx,
+                               const double* __restrict__ s, const double* __restrict__ ds,
+                               double alpha, double* __restrict__ xn, double* __restrict__ sn,
+                               int64_t n) {
+  for (int64_t j = gtid(); j < n; j += gstride()) {
+    xn[j] = __dadd_rn(x[j], __dmul_rn(alpha, dx[j]));
+    sn[j] = __dadd_rn(s[j], __dmul_rn(alpha, ds[j]));
+  }
+}
+
+// out[0] = sigma * (sum / n): the next step's sigma * mu, exactly the host's
+// `sigma * (float(sum) / n)`
+__global__ void sigma_mu_kernel(const double* __restrict__ sum, double n, double sigma,
+                                double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = __dmul_rn(sigma, __ddiv_rn(sum[0], n));
+}
+
 // out = a - b (m-vectors, e.g. infeas = A D^2 A' dy - p)
 __global__ void sub_kernel(const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ out, int64_t n) {
@@ -386,6 +405,19 @@ extern "C" int skb_sqrt_xs_scale(const double* t, const double* x, const double*
                                  int64_t n, void* stream) {
   sqrt_xs_scale_kernel<<<red_grid(n), kRedThreads, 0, (cudaStream_t)stream>>>(t, x, s, v, n);
   LAUNCH_OK;
+}
+
+extern "C" int skb_step_xs(const double* x, const double* dx, const double* s, const double* ds,
+                           double alpha, double* xn, double* sn, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  step_xs_kernel<<<red_grid(n), kRedThreads, 0, (cudaStream_t)stream>>>(x, dx, s, ds, alpha, xn,
+                                                                       sn, n);
+  return skb_launch_status(__func__);
+}
+
+extern "C" int skb_sigma_mu(const double* sum, double n, double sigma, double* out, void* stream) {
+  sigma_mu_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(sum, n, sigma, out);
+  return skb_launch_status(__func__);
 }
 
 extern "C" int skb_axpy(const double* x, double alpha, const double* d, double* y, int64_t n,

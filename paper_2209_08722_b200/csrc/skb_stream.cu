@@ -175,7 +175,38 @@ struct OpIter {  // make_iterate at x + a dx, y_new (=z), s + a ds (ipm_core.py:
 // OpDir and OpGemvRatio, so adx and A (v ./ s) are bitwise the separate passes'.
 struct OpDirV : OpDir {
   static constexpr bool kAxpy2 = true;
-  SKB_DEV double coef2(const Pre& p) const { return ddiv(p.v[2], p.v[1]); }
+  SKB_DEV double coef2(const Pre& p, double) const { return ddiv(p.v[2], p.v[1]); }
+};
+
+// make_iterate's pass at a precomputed (x_new, s_new) plus the NEXT step's
+// build_rhs in the same pass (ipm_core.py:94-102 and :196-206): r_d = A'y_new +
+// s_new - c from the column dot, r_p from the first accumulator (coefficient
+// x_new), and p = A (x_new - smu/s_new [- (x_new/s_new) r_d]) from the second,
+// smu = sigma mu_new read from the device (computed from the same x_new, s_new
+// before the pass). Per element and per lane the same operations in the same
+// order as OpIter's and OpRhs's passes: r_d, r_p and p are bitwise theirs.
+struct OpIterP {
+  static constexpr bool kDot = true, kAxpy = true, kAxpy2 = true;
+  static constexpr int kPre = 3;
+  const double *xn, *sn, *c;
+  const double* smu_dev;
+  int infeasible;
+  double* rd_out;
+  SKB_DEV void load(int64_t j, Pre& p) const {
+    p.v[0] = xn[j];
+    p.v[1] = sn[j];
+    p.v[2] = c[j];
+  }
+  SKB_DEV const double* src(int q) const { return q == 0 ? xn : (q == 1 ? sn : c); }
+  SKB_DEV double rd_of(const Pre& p, double dot) const { return dsub(dadd(dot, p.v[1]), p.v[2]); }
+  SKB_DEV double coef(int64_t, const Pre& p, double) const { return p.v[0]; }
+  SKB_DEV void emit(int64_t j, const Pre& p, double dot, double) const { rd_out[j] = rd_of(p, dot); }
+  SKB_DEV double coef2(const Pre& p, double dot) const {  // OpRhs::coef at (x_new, s_new, r_d)
+    const double smu = *smu_dev;
+    double u = dsub(p.v[0], ddiv(smu, p.v[1]));
+    if (infeasible) u = dsub(u, dmul(ddiv(p.v[0], p.v[1]), rd_of(p, dot)));
+    return u;
+  }
 };
 
 template <class Op, class = void>
@@ -187,8 +218,8 @@ struct Axpy2<Op, std::void_t<decltype(Op::kAxpy2)>> {
   static constexpr bool value = Op::kAxpy2;
 };
 template <class Op>
-SKB_DEV double coef2_of(const Op& op, const Pre& p) {
-  if constexpr (Axpy2<Op>::value) return op.coef2(p);
+SKB_DEV double coef2_of(const Op& op, const Pre& p, double dot) {
+  if constexpr (Axpy2<Op>::value) return op.coef2(p, dot);
   else return 0.0;
 }
 
@@ -282,7 +313,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int q = 0; q < Op::kPre; ++q) pc.v[q] = __shfl_sync(0xffffffffu, pre.v[q], c);
         const double cf = op.coef(c0 + c, pc, dot);
-        const double cf2 = coef2_of(op, pc);
+        const double cf2 = coef2_of(op, pc, dot);
         if (lane == 0) op.emit(c0 + c, pc, dot, cf);
         if (Op::kAxpy) {
 #pragma unroll
@@ -340,7 +371,7 @@ __global__ void __launch_bounds__(256, 1)
       const double cf = op.coef(c0 + c, pc, dot);
       if (lane == 0) op.emit(c0 + c, pc, dot, cf);
       if (Op::kAxpy) {
-        const double cf2 = coef2_of(op, pc);  // OpDirV (z from shared memory frees the room)
+        const double cf2 = coef2_of(op, pc, dot);  // OpDirV (z from shared memory frees the room)
 #pragma unroll
         for (int k = 0; k < R2; ++k) {
           acc[2 * k] = fma(cf, a[k].x, acc[2 * k]);
@@ -550,6 +581,7 @@ template <> struct PreRing<OpDir> { static constexpr bool value = true; };
 template <> struct PreRing<OpIter> { static constexpr bool value = true; };
 template <> struct PreRing<OpRhs> { static constexpr bool value = true; };
 template <> struct PreRing<OpDirV> { static constexpr bool value = true; };
+template <> struct PreRing<OpIterP> { static constexpr bool value = true; };
 
 template <class Op>
 SKB_DEV void prefetch_pre(const Op& op, int64_t j, double* dst) {
@@ -661,7 +693,7 @@ __global__ void __launch_bounds__(256, 1)
       dot = dots[pair * 2] + dots[pair * 2 + 1];
     }
     const double cf = op.coef(j, pre, dot);
-    const double cf2 = coef2_of(op, pre);
+    const double cf2 = coef2_of(op, pre, dot);
     if (producer) op.emit(j, pre, dot, cf);
     if (Op::kAxpy) {
 #pragma unroll
@@ -968,19 +1000,19 @@ extern "C" int skb_directions(const double* A, int64_t m, int64_t n, int64_t lda
   return run_stream(A, lda, (int)m, n, dy, adx, nullptr, op, &ws, (cudaStream_t)stream);
 }
 
-extern "C" int skb_directions_v(const double* A, int64_t m, int64_t n, int64_t lda,
-                                const double* dy, const double* x, const double* s,
-                                const double* v, const double* r_d, double sigma_mu, double* ds,
-                                double* dx, double* atdy, double* adx, double* avs,
-                                void* workspace, size_t ws_bytes, void* stream) {
-  // dense column-stream (m <= 1024) and warp-pair (1024 < m <= 2048) paths: z from
-  // shared memory, which leaves the registers for the second accumulator
+// Two-accumulator passes (OpDirV, OpIterP): dense, m <= 2048 (column stream with
+// z from shared memory, or the warp pair); out1 = sum1 - sub1, out2 = sum2 - sub2
+// (sub2 is applied after out1 is written, so it may be out1). Returns
+// SKB_ERR_UNSUPPORTED where the fused pass does not apply (the caller then runs
+// the two single passes).
+template <class Op>
+static int run_stream2(const double* A, int64_t lda, int64_t m, int64_t n, const double* z,
+                       double* out1, const double* sub1, double* out2, const double* sub2,
+                       const Op& op, skb_ws* ws, cudaStream_t st) {
   if (m < 1 || m > 2 * kPairHalf || n < 1 || lda < m || (lda & 1) || ((uintptr_t)A & 15))
     return SKB_ERR_UNSUPPORTED;
-  SKB_WS;
-  cudaStream_t st = (cudaStream_t)stream;
-  OpDirV op;
-  static_cast<OpDir&>(op) = OpDir{x, s, v, r_d, sigma_mu, ds, dx, atdy};
+  int grid;
+  double* part;
   if (m > 1024) {
     static const bool no_pair = getenv("SKB_NO_PAIR") != nullptr;
     if (no_pair) return SKB_ERR_UNSUPPORTED;
@@ -991,10 +1023,10 @@ extern "C" int skb_directions_v(const double* A, int64_t m, int64_t n, int64_t l
     if (stages < 2) return SKB_ERR_UNSUPPORTED;
     const size_t smem = 512 + kPairPreBytes +
                         std::max((size_t)4 * stages * col_bytes, (size_t)4 * m * 8) + zb;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(skb_num_sms(), (n + 3) / 4));
-    double* part = (double*)skb_ws_take(&ws, (size_t)2 * grid * m * 8);
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>(skb_num_sms(), (n + 3) / 4));
+    part = (double*)skb_ws_take(ws, (size_t)2 * grid * m * 8);
     if (!part) return SKB_ERR_WORKSPACE;
-    auto kern = colpair_kernel<OpDirV>;
+    auto kern = colpair_kernel<Op>;
     static size_t configured = 0;
     if (smem > configured) {
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -1003,35 +1035,55 @@ extern "C" int skb_directions_v(const double* A, int64_t m, int64_t n, int64_t l
       configured = smem;
     }
     const int half = (((int)m + 1) / 2 + 63) / 64 * 64;
-    kern<<<grid, 256, smem, st>>>(A, lda, (int)m, n, stages, half, dy, part, op, nullptr);
-    reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(part, grid, (int)m,
-                                                                      nullptr, adx, nullptr);
-    reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(
-        part + (size_t)grid * m, grid, (int)m, nullptr, avs, nullptr);
-    return skb_launch_status(__func__);
+    kern<<<grid, 256, smem, st>>>(A, lda, (int)m, n, stages, half, z, part, op, nullptr);
+  } else {
+    // the column stays in registers, z comes from shared memory (z in registers
+    // too spills at m = 1000: 2.71 ms against 1.34 ms for OpDirV at c2)
+    const StreamCfg c = stream_cfg((int)m, n, lda);
+    grid = c.grid;
+    part = (double*)skb_ws_take(ws, (size_t)2 * c.grid * m * 8);
+    if (!part) return SKB_ERR_WORKSPACE;
+    int rc;
+    if (m <= 64)
+      rc = launch_r2<1, false>(c, A, lda, (int)m, n, z, part, op, st, nullptr);
+    else if (m <= 128)
+      rc = launch_r2<2, false>(c, A, lda, (int)m, n, z, part, op, st, nullptr);
+    else if (m <= 256)
+      rc = launch_r2<4, false>(c, A, lda, (int)m, n, z, part, op, st, nullptr);
+    else if (m <= 512)
+      rc = launch_r2<8, false>(c, A, lda, (int)m, n, z, part, op, st, nullptr);
+    else
+      rc = launch_r2<16, false>(c, A, lda, (int)m, n, z, part, op, st, nullptr);
+    if (rc) return rc;
   }
-  const StreamCfg c = stream_cfg((int)m, n, lda);
-  double* part = (double*)skb_ws_take(&ws, (size_t)2 * c.grid * m * 8);
-  if (!part) return SKB_ERR_WORKSPACE;
-  int rc;
-  // (z in registers too spills at m = 1000: 2.71 ms against 1.68 ms from shared memory;
-  // the two separate passes take 2.45 ms)
-  if (m <= 64)
-    rc = launch_r2<1, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
-  else if (m <= 128)
-    rc = launch_r2<2, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
-  else if (m <= 256)
-    rc = launch_r2<4, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
-  else if (m <= 512)
-    rc = launch_r2<8, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
-  else
-    rc = launch_r2<16, false>(c, A, lda, (int)m, n, dy, part, op, st, nullptr);
-  if (rc) return rc;
-  reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(part, c.grid, (int)m, nullptr,
-                                                                    adx, nullptr);
+  reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(part, grid, (int)m, sub1,
+                                                                    out1, nullptr);
   reduce_partials_kernel<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(
-      part + (size_t)c.grid * m, c.grid, (int)m, nullptr, avs, nullptr);
-  return skb_launch_status(__func__);
+      part + (size_t)grid * m, grid, (int)m, sub2, out2, nullptr);
+  return skb_launch_status("skb_stream2");
+}
+
+extern "C" int skb_directions_v(const double* A, int64_t m, int64_t n, int64_t lda,
+                                const double* dy, const double* x, const double* s,
+                                const double* v, const double* r_d, double sigma_mu, double* ds,
+                                double* dx, double* atdy, double* adx, double* avs,
+                                void* workspace, size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpDirV op;
+  static_cast<OpDir&>(op) = OpDir{x, s, v, r_d, sigma_mu, ds, dx, atdy};
+  return run_stream2(A, lda, m, n, dy, adx, nullptr, avs, nullptr, op, &ws,
+                     (cudaStream_t)stream);
+}
+
+extern "C" int skb_iterate_rhs(const double* A, int64_t m, int64_t n, int64_t lda,
+                               const double* xn, const double* sn, const double* y_new,
+                               const double* c, const double* smu_dev, int32_t infeasible,
+                               const double* b, double* r_p, double* r_d, double* p,
+                               int32_t p_sub_rp, void* workspace, size_t ws_bytes, void* stream) {
+  SKB_WS;
+  OpIterP op{xn, sn, c, smu_dev, infeasible, r_d};
+  return run_stream2(A, lda, m, n, y_new, r_p, b, p, p_sub_rp ? r_p : nullptr, op, &ws,
+                     (cudaStream_t)stream);
 }
 
 extern "C" int skb_iterate(const double* A, int64_t m, int64_t n, int64_t lda, const double* x,

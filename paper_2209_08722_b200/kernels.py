@@ -252,6 +252,24 @@ def directions_v(A, dy, x, s, v, sigma_mu, ds, dx, adx, avs, atdy=None, r_d=None
     return True
 
 
+def iterate_rhs(A, xn, sn, y_new, c, smu_dev, infeasible: bool, r_p, r_d, p, b=None,
+                p_sub_rp: bool = False) -> bool:
+    """make_iterate's pass at (xn, sn) fused with the next step's build_rhs
+    (skb_iterate_rhs); False where it does not apply (CSC, m > 2048)."""
+    if isinstance(A, SparseDeviceMatrix) or A.m > 2048:
+        return False
+    ws, cap = _ws(A.m)
+    try:
+        _lib.call("skb_iterate_rhs", A.cols, A.m, A.n, A.lda, xn, sn, y_new, c, smu_dev,
+                  1 if infeasible else 0, _p(b), r_p, r_d, p, 1 if p_sub_rp else 0, ws, cap,
+                  stream_ptr())
+    except _lib.SkbError as e:
+        if e.code == -6:  # SKB_ERR_UNSUPPORTED
+            return False
+        raise
+    return True
+
+
 def iterate(A, x, s, y_new, b, c, r_p, r_d, dx=None, ds=None, alpha=0.0, x_out=None,
             s_out=None):
     """make_iterate's A-passes in one sweep (ipm_core.py:94-102)."""

@@ -250,6 +250,29 @@ class DeviceLP:
             self._finish_m(r_p, self.b)
         return xo, so, r_p, r_d
 
+    def iterate_with_rhs(self, x, s, y_new, dx, ds, alpha, sigma, infeasible):
+        """iterate() at the step plus the next step's rhs from the same pass over A
+        (bitwise iterate() followed by rhs() at the new point, whose sigma * mu is
+        formed on the device from the same reduction the host's mu comes from):
+        -> (x_new, s_new, r_p, r_d, p) or None where the fused pass does not apply."""
+        if self.sparse or self.m > 2048:
+            return None
+        xo, so = self.new_n(), self.new_n()
+        _lib.call("skb_step_xs", x, dx, s, ds, float(alpha), xo, so, xo.numel(), stream_ptr())
+        st0 = reduce_call("skb_iter_stats", 5, xo, so, None, xo.numel())
+        self.comm.combine_(st0, (SUM, MIN, MIN, MIN, SUM))
+        smu = torch.empty(1, dtype=F64, device=self.device)
+        _lib.call("skb_sigma_mu", st0, float(self.n), float(sigma), smu, stream_ptr())
+        r_p, r_d, p = self.new_m(), self.new_n(), self.new_m()
+        if not K.iterate_rhs(self.A, xo, so, y_new, self.c, smu, infeasible, r_p, r_d, p,
+                             b=self._sub_arg(self.b),
+                             p_sub_rp=infeasible and not self.comm.active):
+            return None
+        if self.comm.active:
+            self._finish_m(r_p, self.b)
+            self._finish_m(p, r_p if infeasible else None)
+        return xo, so, r_p, r_d, p
+
     # ------------------------------------------------------- reductions
     def vec_stats(self, a, sub=None, global_=True):
         """{sum t^2, sum t, max|t|, min t} of t = a - sub over the global vector."""

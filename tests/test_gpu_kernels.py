@@ -316,3 +316,32 @@ def test_directions_v_fused_bitwise(K, m, n, mode):
                           out[4], atdy=out[3], r_d=r_d)
     for a, b in zip(out, ref):
         assert np.array_equal(_h(a), _h(b))
+
+
+@pytest.mark.parametrize("m,n,mode", [(37, 3001, "feasible"), (1000, 50001, "infeasible"),
+                                      (1000, 20000, "feasible"), (2000, 30000, "infeasible")])
+def test_iterate_rhs_fused_bitwise(K, m, n, mode):
+    """The iterate pass fused with the next step's rhs (skb_step_xs + sigma mu on
+    the device + skb_iterate_rhs) against skb_iterate followed by skb_rhs at the
+    new point with the host's sigma * mu: x_new, s_new, r_p, r_d and p bitwise."""
+    from paper_2209_08722_b200 import _lib
+    from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
+    from paper_2209_08722_b200.runtime import stream_ptr, to_host
+    g, A = _problem(m, n, m + 5)
+    x, s = g.random(n) + 0.2, g.random(n) + 0.2
+    dx, ds = 0.1 * g.standard_normal(n), 0.1 * g.standard_normal(n)
+    y = g.standard_normal(m)
+    b, c = g.standard_normal(m), g.standard_normal(n)
+    lp = DeviceLP.from_host(LinearProgram(A, b, c))
+    alpha, sigma = 0.8125, 0.5
+    inf = mode == "infeasible"
+    fused = lp.iterate_with_rhs(_t(x), _t(s), _t(y), _t(dx), _t(ds), alpha, sigma, inf)
+    assert fused is not None
+    xo, so, r_p, r_d = lp.iterate(_t(x), _t(s), _t(y), dx=_t(dx), ds=_t(ds), alpha=alpha)
+    st = torch.zeros(5, dtype=torch.float64, device="cuda")
+    from paper_2209_08722_b200.lp_model import reduce_call
+    st = reduce_call("skb_iter_stats", 5, xo, so, None, xo.numel())
+    mu = float(to_host(st)[0]) / n
+    p = lp.rhs(xo, so, sigma * mu, r_d=r_d if inf else None, r_p=r_p if inf else None)
+    for a, bb in zip(fused, (xo, so, r_p, r_d, p)):
+        assert np.array_equal(_h(a), _h(bb))
