@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kEllSkT, 1)
                           const int32_t* __restrict__ mem_e, double vmag, int s, int w, int m,
                           unsigned int* __restrict__ counter, double* __restrict__ X,
                           int64_t ldx) {
-  __shared__ int sb, slong, spend;
+  __shared__ int sb;
   extern __shared__ __align__(16) double acc[];  // m doubles, then m int32 bids
   int* bid = reinterpret_cast<int*>(acc + m);
   const int tid = threadIdx.x;
@@ -778,6 +778,278 @@ __global__ void __launch_bounds__(kEllSkT, 1)
     }
   }
 }
+
+// ---- CSC A through ELL records, one counting sort by row per bucket (the
+// default for 2048 < m <= ~40,000; the bid-round kernel above stays behind
+// SKB_CSC_SKETCH_BIDS=1). Up to kRowsT * kRowsM members of a bucket at a time:
+//   1. each thread loads its members' 64-byte records (all loads in flight
+//      together), forms the terms t = fl(fl(A_ij d_j) v) in registers and
+//      takes a ticket in its row with a packed-u16 shared atomic (count);
+//   2. one block scan turns the counts into row offsets;
+//   3. each term goes to slot offset(row) + ticket with its member index (the
+//      order inside a row is arbitrary);
+//   4. rows are summed straight into X (no accumulator in shared memory):
+//      0 + t1 + t2 does not depend on the order of t1 and t2 (fl(0 + t) = t up
+//      to the sign of zero, fl(a + b) = fl(b + a)), so rows with at most two
+//      terms are summed at once, two rows per thread; rows with three or more
+//      are queued and summed by one thread each in ascending member order.
+// Every (row, bucket) sum is the ascending-j left-to-right fl-sum, bit-exact,
+// with records read once and no rounds. Later chunks of a large bucket
+// continue each row from X; a chunk holding a column longer than a record
+// runs member by member on X in place.
+constexpr int kRowsT = 768, kRowsM = 3;  // threads, members per thread
+constexpr size_t kRowsSmemMax = 227 * 1024 - 1024;  // + the static shared words
+
+static size_t rows_hard_entries(int m) {  // per-warp lists: every row a warp covers
+  const size_t W = (size_t)(m + 1) / 2;
+  return (size_t)(kRowsT / 32) * ((W + kRowsT - 1) / kRowsT) * 64;
+}
+static size_t rows_fixed_bytes(int m) {
+  const size_t words = (size_t)(m + 1) / 2 + 1;
+  return ((words * 4 + 15) & ~(size_t)15) + ((rows_hard_entries(m) * 2 + 15) & ~(size_t)15);
+}
+constexpr int kRowsCap = kRowsT * kRowsM * 5;  // terms per chunk (< 2^16)
+static size_t rows_smem_bytes(int m) { return rows_fixed_bytes(m) + (size_t)kRowsCap * 10; }
+SKB_DEV int half16(uint32_t wv, int r) { return (int)((wv >> ((r & 1) * 16)) & 0xFFFFu); }
+SKB_DEV uint32_t row_inc(int r) { return 1u << ((r & 1) * 16); }
+
+__global__ void __launch_bounds__(kRowsT, 1)
+    csc_sketch_rows_kernel(const SkEll* __restrict__ ell, const int64_t* __restrict__ colptr,
+                           const int32_t* __restrict__ rowidx, const double* __restrict__ av,
+                           const uint64_t* __restrict__ start, const int32_t* __restrict__ mem_e,
+                           double vmag, int s, int w, int m, unsigned int* __restrict__ counter,
+                           double* __restrict__ X, int64_t ldx) {
+  extern __shared__ __align__(16) unsigned char rs_sm[];
+  const int W = (m + 1) / 2;
+  uint32_t* offw = reinterpret_cast<uint32_t*>(rs_sm);  // row r: half (r & 1) of word r >> 1
+  uint16_t* hard = reinterpret_cast<uint16_t*>(rs_sm + (((size_t)(W + 1) * 4 + 15) & ~(size_t)15));
+  const int hcap = ((W + kRowsT - 1) / kRowsT) * 64;  // this warp's list capacity
+  double* Sv = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(hard) +
+                                         (((size_t)(kRowsT / 32) * hcap * 2 + 15) & ~(size_t)15));
+  uint16_t* Sm = reinterpret_cast<uint16_t*>(Sv + kRowsCap);
+  __shared__ int s_b;
+  __shared__ int s_wtot[32];
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kNW = kRowsT / 32;
+  constexpr int cm = kRowsT * kRowsM;  // members per chunk
+  for (;;) {
+    __syncthreads();  // the previous bucket is done with offw / hard / S
+    if (tid == 0) s_b = (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int b = s_b;
+    if (b >= w) break;
+    const uint64_t e0 = start[b], e1 = start[b + 1];
+    double* xb = X + (int64_t)b * ldx;
+    const int64_t nmem = (int64_t)(e1 - e0);
+    if (nmem == 0) {
+      for (int r = tid; r < m; r += kRowsT) xb[r] = 0.0;
+      continue;
+    }
+    for (int64_t c0 = 0; c0 < nmem; c0 += cm) {
+      const int nc = (int)min((int64_t)cm, nmem - c0);
+      const bool first = c0 == 0;
+      const int32_t* mc = mem_e + e0 + c0;
+      for (int i = tid; i <= W; i += kRowsT) offw[i] = 0u;
+      // ---- 1. records (member i = tid + k * kRowsT), terms and tickets in registers
+      SkEll rec[kRowsM];
+      uint32_t code[kRowsM];
+      bool has[kRowsM];
+      bool lng = false;
+#pragma unroll
+      for (int k = 0; k < kRowsM; ++k) {
+        const int i = tid + k * kRowsT;
+        has[k] = i < nc;
+        code[k] = has[k] ? (uint32_t)mc[i] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kRowsM; ++k)
+        if (has[k]) rec[k] = ell[(int64_t)(code[k] & 0x7FFFFFFFu) / s];
+#pragma unroll
+      for (int k = 0; k < kRowsM; ++k) lng |= has[k] && rec[k].cnt > 5;
+      __syncthreads();  // offw zeroed
+      if (!__syncthreads_or(lng)) {
+        uint32_t tk[kRowsM][5];  // row | ticket << 16 (0xFFFF: no term)
+        double tv[kRowsM][5];
+#pragma unroll
+        for (int k = 0; k < kRowsM; ++k) {
+          const double v = (code[k] & 0x80000000u) ? -vmag : vmag;
+#pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            tk[k][q] = 0xFFFFu;
+            if (has[k] && q < rec[k].cnt) {
+              const int row = rec[k].row[q];
+              tk[k][q] = (uint32_t)row |
+                         ((uint32_t)half16(atomicAdd(&offw[row >> 1], row_inc(row)), row) << 16);
+              tv[k][q] = __dmul_rn(__dmul_rn(rec[k].val[q], rec[k].d), v);
+            }
+          }
+        }
+        __syncthreads();
+        // ---- 2. exclusive scan of the counts (thread t owns a run of words)
+        const int per = (W + kRowsT - 1) / kRowsT;
+        const int w0 = min(W, tid * per), w1 = min(W, w0 + per);
+        int sum = 0;
+        for (int i = w0; i < w1; ++i) {
+          const uint32_t v = offw[i];
+          sum += (int)(v & 0xFFFFu) + (int)(v >> 16);
+        }
+        int inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_wtot[warp] = inc;
+        __syncthreads();
+        const int wt = lane < kNW ? s_wtot[lane] : 0;
+        int winc = wt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, winc, o);
+          if (lane >= o) winc += y;
+        }
+        int run = __shfl_sync(FULL, winc - wt, warp) + inc - sum;
+        for (int i = w0; i < w1; ++i) {
+          const uint32_t v = offw[i];
+          const uint32_t lo = (uint32_t)run;
+          run += (int)(v & 0xFFFFu);
+          offw[i] = lo | ((uint32_t)run << 16);
+          run += (int)(v >> 16);
+        }
+        if (tid == kRowsT - 1) offw[W] = (uint32_t)run;  // end of the last row (m odd: half 0)
+        __syncthreads();
+        // ---- 3. terms to their slots
+#pragma unroll
+        for (int k = 0; k < kRowsM; ++k)
+#pragma unroll
+          for (int q = 0; q < 5; ++q)
+            if (tk[k][q] != 0xFFFFu) {
+              const int row = (int)(tk[k][q] & 0xFFFFu);
+              const int slot = half16(offw[row >> 1], row) + (int)(tk[k][q] >> 16);
+              Sv[slot] = tv[k][q];
+              Sm[slot] = (uint16_t)(tid + k * kRowsT);
+            }
+        __syncthreads();
+        // ---- 4. two rows per thread (word k = rows 2k, 2k+1; offw[W] = total);
+        // order-free rows now, rows with more terms queued
+        const int lim = first ? 2 : 1;
+        uint16_t* hl = hard + warp * hcap;  // this warp's queued rows
+        int nh = 0;
+#pragma unroll 1
+        for (int k0 = 0; k0 < W; k0 += kRowsT) {
+          const int k = k0 + tid;
+          bool q0 = false, q1 = false;
+          if (k < W) {
+            const uint32_t v = offw[k], vn = offw[k + 1];
+            const int s0 = (int)(v & 0xFFFFu), s1 = (int)(v >> 16), en = (int)(vn & 0xFFFFu);
+            const int n0 = s1 - s0, n1 = en - s1;  // row 2k + 1 = m (m odd): n1 = 0
+            q0 = n0 > lim;
+            q1 = n1 > lim;
+            double* xp = xb + 2 * k;
+            if (first) {  // hard rows get a placeholder here, their sum below
+              double x0 = 0.0, x1 = 0.0;
+              if (n0 >= 1 && !q0) x0 = __dadd_rn(x0, Sv[s0]);
+              if (n0 == 2) x0 = __dadd_rn(x0, Sv[s0 + 1]);
+              if (n1 >= 1 && !q1) x1 = __dadd_rn(x1, Sv[s1]);
+              if (n1 == 2) x1 = __dadd_rn(x1, Sv[s1 + 1]);
+              if (2 * k + 1 < m)
+                *reinterpret_cast<double2*>(xp) = make_double2(x0, x1);
+              else
+                xp[0] = x0;
+            } else {
+              if (n0 == 1) xp[0] = __dadd_rn(xp[0], Sv[s0]);
+              if (n1 == 1) xp[1] = __dadd_rn(xp[1], Sv[s1]);
+            }
+          }
+          const unsigned m0 = __ballot_sync(FULL, q0), m1 = __ballot_sync(FULL, q1);
+          const unsigned lt = (1u << lane) - 1u;
+          if (q0) hl[nh + __popc(m0 & lt)] = (uint16_t)(2 * k);
+          if (q1) hl[nh + __popc(m0) + __popc(m1 & lt)] = (uint16_t)(2 * k + 1);
+          nh += __popc(m0) + __popc(m1);
+        }
+        __syncwarp();  // the placeholders above are overwritten by other lanes below
+        // this warp's queued rows, one per lane, terms in ascending member order: a
+        // sorting network over eight (member, term) pairs, selection beyond eight
+        for (int k0 = 0; k0 < nh; k0 += 32) {
+          const int k = k0 + lane;
+          int r = 0, lo = 0, c = 0;
+          if (k < nh) {
+            r = hl[k];
+            const uint32_t v = offw[r >> 1];
+            lo = half16(v, r);
+            const int hi = (r & 1) ? (int)(offw[(r >> 1) + 1] & 0xFFFFu) : (int)(v >> 16);
+            c = hi - lo;
+          }
+          double x = 0.0;
+          if (k < nh && !first) x = xb[r];
+          if (__any_sync(FULL, c > 8)) {
+            int prev = -1;
+            for (int u = 0; u < c; ++u) {  // the next member in ascending order
+              int best = 0x7FFFFFFF, bi = lo;
+              for (int q = lo; q < lo + c; ++q) {
+                const int mm = Sm[q];
+                if (mm > prev && mm < best) {
+                  best = mm;
+                  bi = q;
+                }
+              }
+              x = __dadd_rn(x, Sv[bi]);
+              prev = best;
+            }
+          } else {
+            int key[8];
+            double val[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              key[q] = q < c ? (int)Sm[lo + q] : 0x10000 + q;
+              val[q] = q < c ? Sv[lo + q] : 0.0;
+            }
+            // Batcher odd-even merge sort, 8 inputs (19 compare-exchanges)
+            auto cx = [&](int a, int b) {
+              const bool sw = key[a] > key[b];
+              const int ka = key[a];
+              const double va = val[a];
+              key[a] = sw ? key[b] : key[a];
+              val[a] = sw ? val[b] : val[a];
+              key[b] = sw ? ka : key[b];
+              val[b] = sw ? va : val[b];
+            };
+            cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7);
+            cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7);
+            cx(1, 2); cx(5, 6);
+            cx(0, 4); cx(1, 5); cx(2, 6); cx(3, 7);
+            cx(2, 4); cx(3, 5);
+            cx(1, 2); cx(3, 4); cx(5, 6);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < c) x = __dadd_rn(x, val[q]);
+          }
+          if (k < nh) xb[r] = x;
+        }
+      } else {
+        // a column longer than a record: member by member, rows split, X in place
+        if (first) {
+          for (int r = tid; r < m; r += kRowsT) xb[r] = 0.0;
+          __syncthreads();
+        }
+        for (int i = 0; i < nc; ++i) {
+          const uint32_t cd = (uint32_t)mc[i];
+          const int64_t j = (int64_t)(cd & 0x7FFFFFFFu) / s;
+          const double v = (cd & 0x80000000u) ? -vmag : vmag;
+          const double dj = ell[j].d;
+          const int64_t a0 = colptr[j], a1 = colptr[j + 1];
+          for (int64_t e = a0 + tid; e < a1; e += kRowsT) {  // a column's rows are distinct
+            const int row = rowidx[e];
+            xb[row] = __dadd_rn(xb[row], __dmul_rn(__dmul_rn(av[e], dj), v));
+          }
+          __syncthreads();
+        }
+      }
+      __syncthreads();  // the next chunk reuses offw / S / hard and reads X
+    }
+  }
+}
 }  // namespace skb
 
 extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx,
@@ -793,7 +1065,29 @@ extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx
   unsigned int* counter;
   int rc = bucket_sort(cols, vals, n, s, w, &ws, st, &start, &mem_e, &counter);
   if (rc) return rc;
-  if (ell && m > 2048 && m <= 65535 && n > 0 && !getenv("SKB_CSC_SKETCH_L2")) {
+  const bool use_ell = ell && m > 2048 && m <= 65535 && n > 0 && !getenv("SKB_CSC_SKETCH_L2");
+  // s = 1 (500 members a bucket at c4): the bid-round kernel is faster
+  // (2.93 vs 3.60 ms per c4 apply); s >= 2: the row-sorting kernel (s = 4:
+  // 7.26 vs 7.71 ms), profiles/r02_csc_sketch_c4.txt
+  const bool bids = getenv("SKB_CSC_SKETCH_BIDS") != nullptr || s == 1;
+  if (use_ell && !bids && !(ldx & 1) && rows_smem_bytes((int)m) <= kRowsSmemMax) {
+    const size_t smem = rows_smem_bytes((int)m);
+    static size_t conf_r = 0;
+    if (smem > conf_r) {
+      if (cudaFuncSetAttribute(csc_sketch_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return SKB_ERR_UNSUPPORTED;
+      conf_r = smem;
+    }
+    const double vmag = 1.0 / std::sqrt((double)s);  // as below
+    ell_set_d_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((SkEll*)ell, d, n);
+    const int grid = std::min(skb_num_sms(), (int)w);
+    csc_sketch_rows_kernel<<<grid, kRowsT, smem, st>>>((const SkEll*)ell, colptr, rowidx, av,
+                                                       start, mem_e, vmag, s, w, (int)m, counter,
+                                                       X, ldx);
+    return skb_launch_status(__func__);
+  }
+  if (use_ell) {
     const size_t smem = (size_t)m * 12;  // accumulator + bids
     static size_t conf_e = 0;
     if (smem > conf_e) {

@@ -89,11 +89,13 @@ def test_csc_sketch_apply_bit_exact(K):
     assert np.array_equal(_h(X.cols)[:, :3000].T, ref)
 
 
-@pytest.mark.parametrize("kernel", ["ell", "l2"])
+@pytest.mark.parametrize("kernel", ["ell", "bids", "l2"])
 @pytest.mark.parametrize("m,n,k,w,s,radix", [(2500, 10_000, 5, 600, 4, False),
                                               (2600, 8000, 12, 500, 3, False),
                                               (2500, 10_000, 5, 600, 4, True),
-                                              (2500, 10_000, 0, 700, 4, False)])
+                                              (2500, 10_000, 0, 700, 4, False),
+                                              (2500, 20_000, 5, 4, 2, False),
+                                              (2500, 20_000, 0, 3, 2, False)])
 def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix, kernel):
     """m > 2048 takes the warp-per-bucket L2 kernel: few buckets (many repeated
     rows per member chunk -> the ordered path) and columns longer than its
@@ -101,14 +103,18 @@ def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix, kern
     against the C restatement of scipy's summation order. radix: the bucket
     order from the CUB radix sort (its default from 2^20 entries, forced here)
     instead of the counting sort. kernel: the ELL-record kernel (one CTA per
-    bucket, radix-sorted batches; k = 0: ragged columns of 0..12 entries, the long
-    ones split a batch) or the L2 kernel (SKB_CSC_SKETCH_L2=1)."""
+    bucket, rows binned to owner warps; k = 0: ragged columns of 0..12 entries, the
+    long ones split a batch), its bid-round variant (SKB_CSC_SKETCH_BIDS=1) or the L2
+    kernel (SKB_CSC_SKETCH_L2=1). w = 3-4: 1e4+ members per bucket, several chunks of the
+    row-sorting kernel (later chunks continue each row from X)."""
     from paper_2209_08722_b200 import sketching as S
     from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
     if radix:
         monkeypatch.setenv("SKB_BUCKET_RADIX", "1")
     if kernel == "l2":
         monkeypatch.setenv("SKB_CSC_SKETCH_L2", "1")
+    if kernel == "bids":
+        monkeypatch.setenv("SKB_CSC_SKETCH_BIDS", "1")
     if k == 0:  # ragged: mostly short columns, some longer than an ELL record
         g0 = np.random.Generator(np.random.Philox(m + n))
         lens = np.where(g0.random(n) < 0.9, g0.integers(0, 6, n), g0.integers(6, 13, n))
