@@ -278,9 +278,18 @@ extern "C" int skb_pcg_solve(const double* A, int64_t m, int64_t n, int64_t lda,
   PcgState h;
   skb_readback rb(st);
   rb.add(&h, S, sizeof(PcgState));
+  // the trace rides the same pinned readback (a pageable cudaMemcpy after the
+  // sync cost ~1 ms per solve on the c2 timeline)
+  double tbuf[400];
+  const bool tr_pinned = trace_host && t_max + 1 <= 400;
+  if (tr_pinned) rb.add(tbuf, trace, sizeof(double) * (size_t)(t_max + 1));
   if (rb.sync() != cudaSuccess) return SKB_ERR_CUDA;
   if (trace_host && h.iters + 1 > 0) {
-    cudaMemcpy(trace_host, trace, sizeof(double) * (size_t)(h.iters + 1), cudaMemcpyDeviceToHost);
+    if (tr_pinned)
+      memcpy(trace_host, tbuf, sizeof(double) * (size_t)(h.iters + 1));
+    else
+      cudaMemcpy(trace_host, trace, sizeof(double) * (size_t)(h.iters + 1),
+                 cudaMemcpyDeviceToHost);
   }
   out_host[0] = h.iters;
   out_host[1] = h.converged;
