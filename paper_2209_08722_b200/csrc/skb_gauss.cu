@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(32 * kZChainWarps)
     zig_chain_kernel(uint64_t k0, uint64_t k1, uint64_t P0, uint64_t base,
                      const uint32_t* __restrict__ bits, int64_t tiles,
                      uint32_t* __restrict__ gskip, uint32_t* __restrict__ gacc,
-                     uint64_t* __restrict__ cnt, int* __restrict__ err) {
+                     uint64_t* __restrict__ cnt, int* __restrict__ err,
+                     double* __restrict__ vals, double sqrtw) {
   __shared__ ZigTables T;
   __shared__ ZigChainWarp W[kZChainWarps];
   zig_load_tables(&T);
@@ -336,6 +337,11 @@ __global__ void __launch_bounds__(32 * kZChainWarps)
         const bool ok = zig_slow(T, k0, k1, q, out64(k0, k1, q), &v, &len);
         S.len[i] = (uint8_t)min(len, 255);
         S.ok[i] = ok;
+        // stored-values mode: an accepted attempt's value goes into its start
+        // position's slot (a slow position: K9a's fast value there is unused),
+        // so the emit pass never recomputes a slow attempt (tiles evaluating
+        // the same attempt write the same value)
+        if (vals && ok) vals[q - base] = div_by(v, sqrtw, __drcp_rn(sqrtw));
       }
       __syncwarp();
       // prefix max of attempt ends (as if every entry were an attempt)
@@ -409,8 +415,8 @@ __global__ void __launch_bounds__(kZThreads, 3)
   const double rsqrtw = __drcp_rn(sqrtw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __syncthreads();
-  int par = 0;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, par ^= 1) {
+  int par = 0;  // warp_sum buffer: flips per processed tile (skipped tiles have no barrier)
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint64_t t0 = P0 + (uint64_t)tile * kZTile;
     const uint64_t my0 = t0 + (uint64_t)tid * kZPer;
     const uint64_t base = offs[tile];
@@ -465,12 +471,13 @@ __global__ void __launch_bounds__(kZThreads, 3)
 #pragma unroll
     for (int i = 0, k = 0; i < kZPer; ++i) {
       if (outm & (1u << i)) {
-        if (!((ac >> i) & 1u)) buf[off + k] = vals ? vv[i] : div_by(vv[i], sqrtw, rsqrtw);
+        if (vals || !((ac >> i) & 1u)) buf[off + k] = vals ? vv[i] : div_by(vv[i], sqrtw, rsqrtw);
         ++k;
       }
     }
     // accepted slow attempts (rare): recompute their values in a rolled loop
-    for (uint32_t rest = ac; rest; rest &= rest - 1) {
+    // (stored-values mode: K9b already put them into vals)
+    for (uint32_t rest = vals ? 0u : ac; rest; rest &= rest - 1) {
       const int i = __ffs(rest) - 1;
       const uint64_t q = my0 + i;
       double v;
@@ -479,11 +486,99 @@ __global__ void __launch_bounds__(kZThreads, 3)
       buf[off + __popc(outm & ((1u << i) - 1u))] = div_by(v, sqrtw, rsqrtw);
     }
     __syncwarp();
-    for (uint32_t p = lane; p < wcount; p += 32) {
-      const uint64_t idx = wfirst + p;
-      if (idx >= lo && idx < need) out[idx - lo] = buf[p];
-    }
+    // the warp's slice of [lo, need): 32-bit offsets from one 64-bit base
+    const uint32_t p_lo =
+        wfirst >= lo ? 0u : (lo - wfirst < wcount ? (uint32_t)(lo - wfirst) : wcount);
+    const uint32_t p_hi =
+        wfirst >= need ? 0u : (need - wfirst < wcount ? (uint32_t)(need - wfirst) : wcount);
+    double* ow = out + (int64_t)(wfirst - lo);  // only dereferenced at p in [p_lo, p_hi)
+    for (uint32_t p = p_lo + lane; p < p_hi; p += 32) ow[p] = buf[p];
     __syncwarp();
+    par ^= 1;
+  }
+}
+
+// ---- K9d in the stored-values mode: every value it emits (fast ones from K9a,
+// accepted slow ones from K9b) is already in vals, so the pass is a stream
+// compaction; the next tile's values are loaded while this tile's draws are
+// stored (the two-phase loop above left the loads idle during the stores).
+struct ZigPre {
+  double v[kZPer];
+  uint32_t slow, sk, ac;
+  uint64_t base, tcount;
+};
+
+__global__ void __launch_bounds__(kZThreads, 3)
+    zig_emit_vals_kernel(uint64_t P0, int64_t tiles, const uint32_t* __restrict__ gskip,
+                         const uint32_t* __restrict__ gacc, const uint64_t* __restrict__ offs,
+                         uint64_t lo, uint64_t need, double* __restrict__ out,
+                         const uint32_t* __restrict__ bits, const double* __restrict__ vals,
+                         uint64_t vbase) {
+  __shared__ uint32_t warp_sum[2][kZThreads / 32];
+  __shared__ double wbuf[kZThreads / 32][32 * kZPer];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto fetch = [&](int64_t tile, ZigPre& f) {
+    f.base = offs[tile];
+    f.tcount = offs[tile + 1] - f.base;
+    const uint64_t rel = P0 + (uint64_t)tile * kZTile + (uint64_t)tid * kZPer - vbase;
+    f.slow = (bits[rel >> 5] >> (rel & 31)) & 0xffffu;
+    f.sk = (gskip[tile * kZWords + (tid >> 1)] >> ((tid & 1) * 16)) & 0xffffu;
+    f.ac = (gacc[tile * kZWords + (tid >> 1)] >> ((tid & 1) * 16)) & 0xffffu;
+    const double2* src = reinterpret_cast<const double2*>(vals + rel);
+#pragma unroll
+    for (int i = 0; i < kZPer / 2; ++i) {
+      const double2 t2 = src[i];
+      f.v[2 * i] = t2.x;
+      f.v[2 * i + 1] = t2.y;
+    }
+  };
+  ZigPre cur;
+  int64_t tile = blockIdx.x;
+  if (tile < tiles) fetch(tile, cur);
+  int par = 0;
+  for (; tile < tiles; tile += gridDim.x) {
+    const int64_t nt = tile + gridDim.x;
+    const uint64_t base = cur.base, tcount = cur.tcount;
+    if (base >= need || base + tcount <= lo) {  // uniform across the CTA
+      if (nt < tiles) fetch(nt, cur);
+      continue;
+    }
+    const uint32_t outm = ((~cur.slow & 0xffffu) & ~cur.sk) | cur.ac;
+    const uint32_t c = __popc(outm);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_sum[par][warp] = incl;
+    __syncthreads();
+    uint32_t wbase = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kZThreads / 32; ++w2)
+      if (w2 < warp) wbase += warp_sum[par][w2];
+    const uint64_t first = base + wbase + incl - c;
+    const uint64_t wfirst = __shfl_sync(0xffffffffu, first, 0);
+    const uint32_t wcount = __shfl_sync(0xffffffffu, incl, 31);
+    double* buf = wbuf[warp];
+    const uint32_t off = (uint32_t)(first - wfirst);
+#pragma unroll
+    for (int i = 0, k = 0; i < kZPer; ++i) {
+      if (outm & (1u << i)) {
+        buf[off + k] = cur.v[i];
+        ++k;
+      }
+    }
+    if (nt < tiles) fetch(nt, cur);  // in flight during the stores below
+    __syncwarp();
+    const uint32_t p_lo =
+        wfirst >= lo ? 0u : (lo - wfirst < wcount ? (uint32_t)(lo - wfirst) : wcount);
+    const uint32_t p_hi =
+        wfirst >= need ? 0u : (need - wfirst < wcount ? (uint32_t)(need - wfirst) : wcount);
+    double* ow = out + (int64_t)(wfirst - lo);
+    for (uint32_t p = p_lo + lane; p < p_hi; p += 32) ow[p] = buf[p];
+    __syncwarp();
+    par ^= 1;
   }
 }
 
@@ -522,9 +617,12 @@ static int zig_generate(uint64_t k0, uint64_t k1, uint64_t P0, uint64_t P1, uint
   zig_chain_kernel<<<(unsigned)std::min<int64_t>((tiles + kZChainWarps - 1) / kZChainWarps,
                                                  16LL * sms),
                      32 * kZChainWarps, 0, st>>>(k0, k1, P0, base, bits, tiles, gskip, gacc, cnt,
-                                                 err);
+                                                 err, vals, __builtin_sqrt((double)w));
   cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, offs, (int)(tiles + 1), st);
-  if (need > lo)
+  if (need > lo && vals)
+    zig_emit_vals_kernel<<<(unsigned)std::min<int64_t>(tiles, 8LL * sms), kZThreads, 0, st>>>(
+        P0, tiles, gskip, gacc, offs, lo, need, out, bits, vals, base);
+  else if (need > lo)
     zig_emit_kernel<<<(unsigned)std::min<int64_t>(tiles, 8LL * sms), kZThreads, 0, st>>>(
         k0, k1, P0, tiles, gskip, gacc, offs, lo, need, __builtin_sqrt((double)w), out, bits,
         vals, base);

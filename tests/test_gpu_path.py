@@ -398,11 +398,15 @@ def test_config1_lockstep_s1(P):
     assert strict_steps >= 10
 
 
-def test_gaussian_sketch_bit_exact(P):
+@pytest.mark.parametrize("store", ["1", "0"])
+def test_gaussian_sketch_bit_exact(P, monkeypatch, store):
     """K9: W = standard_normal((n, w)) / sqrt(w) reproduced bit for bit, incl. the
     ziggurat's wedge/tail slow paths (~0.7% of draws; the tail's log1p is glibc's,
-    restated in csrc/skb_gauss.cu) and a row-block slice."""
+    restated in csrc/skb_gauss.cu) and a row-block slice. store: the stored-values
+    mode (the classify pass keeps the fast values, the chain pass the accepted slow
+    ones) or the recomputing one (SKB_ZIG_STORE=0)."""
     import hashlib
+    monkeypatch.setenv("SKB_ZIG_STORE", store)
     from paper_2209_08722_b200 import sketching as S
     with open(os.path.join(GOLDEN, "gaussian_traces.json")) as f:
         gold = json.load(f)
