@@ -155,16 +155,26 @@ __global__ void scatter_rows_kernel(const uint32_t* vals, const int64_t* rows, i
 }
 
 // Signs: Lemire with bound 2 never rejects; sign = 2*(W>>31) - 1, val = sign/sqrt(s).
+// One thread per Philox block (8 consecutive 32-bit words): one Philox call for
+// its 8 signs (one call per sign computed the same block 8 times over), and
+// sign / sqrt(s) = +-(1 / sqrt(s)) exactly, so the quotient is formed once.
 __global__ void sign_kernel(uint64_t k0, uint64_t k1, uint64_t q0, int64_t cnt, int s,
                             double* vals) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= cnt) return;
-  const uint64_t q = q0 + i;
-  u64x4 o = philox4x64_10((q >> 3) + 1, 0, 0, 0, k0, k1);
-  const uint64_t v = o.v[(q >> 1) & 3];
-  const uint32_t wd = (q & 1) ? (uint32_t)(v >> 32) : (uint32_t)v;
-  const double sign = __dsub_rn(__dmul_rn((double)(wd >> 31), 2.0), 1.0);
-  vals[i] = __ddiv_rn(sign, __dsqrt_rn((double)s));
+  const uint64_t blk = (q0 >> 3) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t qa = blk * 8 > q0 ? blk * 8 : q0;
+  const uint64_t qe = q0 + (uint64_t)cnt, qb = blk * 8 + 8 < qe ? blk * 8 + 8 : qe;
+  if (qa >= qb) return;
+  const u64x4 o = philox4x64_10(blk + 1, 0, 0, 0, k0, k1);
+  const double vmag = __ddiv_rn(1.0, __dsqrt_rn((double)s));
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint64_t q = blk * 8 + u;
+    if (q >= qa && q < qb) {
+      const uint64_t v = o.v[u >> 1];
+      const uint32_t wd = (u & 1) ? (uint32_t)(v >> 32) : (uint32_t)v;
+      vals[q - q0] = (wd >> 31) ? vmag : -vmag;
+    }
+  }
 }
 
 // 2s >= w branch: cols[j] = argsort(random((n, w))[j])[:s]. next_double =
@@ -320,7 +330,10 @@ extern "C" int skb_sparse_embedding(uint64_t key0, uint64_t key1, int64_t n, int
     }
   }
   const int64_t cnt = n * (int64_t)s;
-  sign_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(key0, key1, pos, cnt, s, vals);
+  if (cnt > 0) {
+    const int64_t nblk = (int64_t)(((pos + (uint64_t)cnt - 1) >> 3) - (pos >> 3)) + 1;
+    sign_kernel<<<(unsigned)((nblk + 255) / 256), 256, 0, st>>>(key0, key1, pos, cnt, s, vals);
+  }
   pos += (uint64_t)cnt;
   if (words_used) *words_used = pos;
   return skb_launch_status(__func__);
