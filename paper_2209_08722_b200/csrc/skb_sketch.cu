@@ -1156,8 +1156,11 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
   const size_t col_bytes = (size_t)lda * 8;
   // tuning knobs (development): CTAs per SM and ring depth
   // Two CTAs per SM (two producers per SM): 1.73 -> 1.32 ms at c2 (round-1 sweep).
-  static const int cps_env = getenv("SKB_SKETCH_CPS") ? atoi(getenv("SKB_SKETCH_CPS")) : 2;
-  const int ctas_per_sm = m <= 2048 ? cps_env : 1;  // large m: one CTA (register budget)
+  // CTAs (bulk-copy producers) per SM: 4 for m <= 1024 (c2 s = 4: 4.91 -> 4.72 ms with 6
+  // stages each, s = 1: 1.289 -> 1.279 ms; sweep in profiles/r02_sketch_s4_analysis.txt),
+  // 2 up to m = 2048, one CTA above (register budget)
+  static const int cps_env = getenv("SKB_SKETCH_CPS") ? atoi(getenv("SKB_SKETCH_CPS")) : 0;
+  const int ctas_per_sm = m > 2048 ? 1 : cps_env > 0 ? cps_env : (m <= 1024 ? 4 : 2);
   static const int max_stages = getenv("SKB_SKETCH_STAGES") ? atoi(getenv("SKB_SKETCH_STAGES")) : 16;
   const size_t budget = (size_t)(200 * 1024) / std::max(1, ctas_per_sm);
   int stages = (int)std::min<size_t>((size_t)max_stages, budget / col_bytes);
