@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(kZThreads, 3)
                          const uint32_t* __restrict__ bits, const double* __restrict__ vals,
                          uint64_t vbase) {
   __shared__ uint32_t warp_sum[2][kZThreads / 32];
-  __shared__ double wbuf[kZThreads / 32][32 * kZPer];
+  __shared__ __align__(16) double wbuf[kZThreads / 32][32 * kZPer + 2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto fetch = [&](int64_t tile, ZigPre& f) {
     f.base = offs[tile];
@@ -560,7 +560,13 @@ __global__ void __launch_bounds__(kZThreads, 3)
     const uint64_t first = base + wbase + incl - c;
     const uint64_t wfirst = __shfl_sync(0xffffffffu, first, 0);
     const uint32_t wcount = __shfl_sync(0xffffffffu, incl, 31);
-    double* buf = wbuf[warp];
+    double* ow = out + (int64_t)(wfirst - lo);  // only dereferenced in [p_lo, p_hi)
+    // stage with the global alignment (buf + sa + p and ow + p agree mod 16 bytes)
+    const uint32_t sa = (uint32_t)((reinterpret_cast<uintptr_t>(ow) >> 3) & 1);
+    double* buf = wbuf[warp] + sa;
+    if (lane == 0)  // the previous tile's bulk store has read the buffer
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
     const uint32_t off = (uint32_t)(first - wfirst);
 #pragma unroll
     for (int i = 0, k = 0; i < kZPer; ++i) {
@@ -575,11 +581,21 @@ __global__ void __launch_bounds__(kZThreads, 3)
         wfirst >= lo ? 0u : (lo - wfirst < wcount ? (uint32_t)(lo - wfirst) : wcount);
     const uint32_t p_hi =
         wfirst >= need ? 0u : (need - wfirst < wcount ? (uint32_t)(need - wfirst) : wcount);
-    double* ow = out + (int64_t)(wfirst - lo);
-    for (uint32_t p = p_lo + lane; p < p_hi; p += 32) ow[p] = buf[p];
-    __syncwarp();
+    // the warp's range as one TMA bulk store (16-byte aligned middle) plus <= 2 edges
+    const uint32_t pa = p_lo + ((reinterpret_cast<uintptr_t>(ow + p_lo) >> 3) & 1);
+    const uint32_t pb = pa < p_hi ? pa + ((p_hi - pa) & ~1u) : pa;
+    if (lane == 0 && p_lo < pa && p_lo < p_hi) ow[p_lo] = buf[p_lo];
+    if (lane == 1 && pb < p_hi) ow[pb] = buf[pb];
+    if (lane == 0 && pb > pa) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(ow + pa), "r"(smem_u32(buf + pa)), "r"((pb - pa) * 8u)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
     par ^= 1;
   }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Draws of the stream positions [P0, P1) (tile multiples), written as
