@@ -1069,8 +1069,12 @@ extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx
   // s = 1 (500 members a bucket at c4): the bid-round kernel is faster
   // (2.93 vs 3.60 ms per c4 apply); s >= 2: the row-sorting kernel (s = 4:
   // 7.26 vs 7.71 ms), profiles/r02_csc_sketch_c4.txt
-  const bool bids = getenv("SKB_CSC_SKETCH_BIDS") != nullptr || s == 1;
-  if (use_ell && !bids && !(ldx & 1) && rows_smem_bytes((int)m) <= kRowsSmemMax) {
+  // Each ELL kernel has a shared-memory ceiling in m (rows: ~27,000, bids: ~18,700);
+  // beyond both the L2 kernel takes the sketch.
+  const bool want_bids = getenv("SKB_CSC_SKETCH_BIDS") != nullptr || s == 1;
+  const bool rows_ok = use_ell && !(ldx & 1) && rows_smem_bytes((int)m) <= kRowsSmemMax;
+  const bool bids_ok = use_ell && (size_t)m * 12 <= 220 * 1024;
+  if (rows_ok && !(want_bids && bids_ok)) {
     const size_t smem = rows_smem_bytes((int)m);
     static size_t conf_r = 0;
     if (smem > conf_r) {
@@ -1087,12 +1091,11 @@ extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx
                                                        X, ldx);
     return skb_launch_status(__func__);
   }
-  if (use_ell) {
+  if (bids_ok) {
     const size_t smem = (size_t)m * 12;  // accumulator + bids
     static size_t conf_e = 0;
     if (smem > conf_e) {
-      if (smem > 220 * 1024 ||
-          cudaFuncSetAttribute(csc_sketch_ell_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      if (cudaFuncSetAttribute(csc_sketch_ell_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem) != cudaSuccess)
         return SKB_ERR_UNSUPPORTED;
       conf_e = smem;

@@ -853,13 +853,113 @@ static int launch_r2(const StreamCfg& c, const double* A, int64_t lda, int m, in
 // Runs the streaming pass. With part_ext != nullptr the per-CTA partials are
 // written there (nparts_out receives their count) and the final reduction is
 // left to the caller (skb_reduce_partials); otherwise out = sum - sub.
+// ---- Dense passes past the staged kernels' shared-memory ceiling (two columns
+// of m doubles per ring no longer fit: m > ~13,900). Two passes over A: (1) one
+// warp per column forms the dot with z (read through L1/L2), the coefficient and
+// the per-column outputs, and keeps the coefficient; (2) CTAs over (row block x
+// column chunk) accumulate cf_j A[:, j] for their rows in registers (coalesced
+// along the column) into per-chunk partials, which the usual fixed-order reduce
+// sums. Deterministic; a robustness path, not a configuration's hot path.
+template <class Op>
+__global__ void __launch_bounds__(256)
+    colwarp_dot_kernel(const double* __restrict__ A, int64_t lda, int m, int64_t n,
+                       const double* __restrict__ z, double* __restrict__ cfo, Op op,
+                       const int* __restrict__ gate) {
+  if (gate && *gate) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); j < n; j += nw) {
+    Pre p;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) p.v[q] = 0.0;
+    op.load(j, p);
+    double dot = 0.0;
+    if (Op::kDot) {
+      const double* col = A + j * lda;
+      for (int r = 2 * lane; r < m; r += 64) {
+        const double2 a = *reinterpret_cast<const double2*>(col + r);
+        dot = fma(a.x, __ldg(&z[r]), dot);
+        if (r + 1 < m) dot = fma(a.y, __ldg(&z[r + 1]), dot);
+      }
+      dot = warp_sum(dot);
+    }
+    const double cf = op.coef(j, p, dot);
+    if (lane == 0) {
+      op.emit(j, p, dot, cf);
+      if (Op::kAxpy) cfo[j] = cf;
+    }
+  }
+}
+
+constexpr int kBlkRows = 4096, kBlkPer = kBlkRows / 256;  // rows per CTA, per thread
+
+__global__ void __launch_bounds__(256)
+    colblk_axpy_kernel(const double* __restrict__ A, int64_t lda, int m, int64_t n,
+                       const double* __restrict__ cf, int64_t chunk, double* __restrict__ part,
+                       const int* __restrict__ gate) {
+  if (gate && *gate) return;
+  const int r0 = blockIdx.y * kBlkRows;
+  const int64_t j0 = (int64_t)blockIdx.x * chunk, j1 = min(n, j0 + chunk);
+  double acc[kBlkPer];
+#pragma unroll
+  for (int k = 0; k < kBlkPer; ++k) acc[k] = 0.0;
+  for (int64_t j = j0; j < j1; ++j) {
+    const double c = __ldg(&cf[j]);
+    const double* col = A + j * lda;
+#pragma unroll
+    for (int k = 0; k < kBlkPer; ++k) {
+      const int r = r0 + threadIdx.x + 256 * k;
+      if (r < m) acc[k] = fma(c, col[r], acc[k]);
+    }
+  }
+  double* o = part + (int64_t)blockIdx.x * m;
+#pragma unroll
+  for (int k = 0; k < kBlkPer; ++k) {
+    const int r = r0 + threadIdx.x + 256 * k;
+    if (r < m) o[r] = acc[k];
+  }
+}
+
+template <class Op>
+static int run_stream_global(const double* A, int64_t lda, int m, int64_t n, const double* z,
+                             double* out, const double* sub, const Op& op, skb_ws* ws,
+                             cudaStream_t st, const int* gate, double* part_ext,
+                             int* nparts_out) {
+  const int rb = (m + kBlkRows - 1) / kBlkRows;
+  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(4 * skb_num_sms() / rb, n));
+  double* cf = nullptr;
+  if (Op::kAxpy) {
+    cf = (double*)skb_ws_take(ws, (size_t)n * 8);
+    if (!cf) return SKB_ERR_WORKSPACE;
+  }
+  if (n > 0)
+    colwarp_dot_kernel<Op><<<(unsigned)std::min<int64_t>(8 * skb_num_sms(), (n + 7) / 8), 256, 0,
+                             st>>>(A, lda, m, n, z, cf, op, gate);
+  if (!Op::kAxpy) return skb_launch_status(__func__);
+  double* part = part_ext;
+  if (!part) {
+    part = (double*)skb_ws_take(ws, (size_t)chunks * m * 8);
+    if (!part) return SKB_ERR_WORKSPACE;
+  }
+  const int64_t chunk = (n + chunks - 1) / chunks;
+  chunks = n > 0 ? (n + chunk - 1) / chunk : 0;
+  if (nparts_out) *nparts_out = (int)chunks;
+  if (chunks > 0)
+    colblk_axpy_kernel<<<dim3((unsigned)chunks, (unsigned)rb), 256, 0, st>>>(A, lda, m, n, cf,
+                                                                            chunk, part, gate);
+  if (!part_ext)
+    reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(part, (int)chunks, m, sub, out, gate);
+  return skb_launch_status(__func__);
+}
+
 template <class Op>
 static int run_stream(const double* A, int64_t lda, int m, int64_t n, const double* z,
                       double* out, const double* sub, const Op& op, skb_ws* ws,
                       cudaStream_t st, const int* gate = nullptr, double* part_ext = nullptr,
                       int* nparts_out = nullptr) {
   if (m < 1 || n < 0 || lda < m || (lda & 1) || ((uintptr_t)A & 15)) return SKB_ERR_ARG;
-  if (m > kCoopMaxM) return SKB_ERR_UNSUPPORTED;
+  if (m > 1024 && (m > kCoopMaxM || coop_cfg(m, n, lda).smem > 225 * 1024))
+    return run_stream_global(A, lda, m, n, z, out, sub, op, ws, st, gate, part_ext, nparts_out);
   if (n == 0) {
     if (nparts_out) *nparts_out = 0;
     if (Op::kAxpy && !part_ext) {
@@ -1233,6 +1333,33 @@ __global__ void __launch_bounds__(kCscThreads)
   for (int i = threadIdx.x; i < m; i += blockDim.x) part[(size_t)blockIdx.x * m + i] = us[i];
 }
 
+// CSC pass for m past the shared-memory kernels' ceiling (z and the partial
+// m-vector no longer fit next to each other): z read through L1/L2, the products
+// added straight into one global m-vector with fp64 RED (arbitration order, as
+// the shared atomics above), then the same reduce / subtract epilogue.
+template <class Op>
+__global__ void __launch_bounds__(256)
+    csc_global_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                      const double* __restrict__ vals, int64_t n, const double* __restrict__ z,
+                      double* __restrict__ acc, Op op, const int* __restrict__ gate) {
+  if (gate && *gate) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    Pre p;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) p.v[q] = 0.0;
+    op.load(j, p);
+    const int64_t e0 = colptr[j], e1 = colptr[j + 1];
+    double dot = 0.0;
+    if (Op::kDot)
+      for (int64_t e = e0; e < e1; ++e) dot = fma(vals[e], __ldg(&z[rowidx[e]]), dot);
+    const double cf = op.coef(j, p, dot);
+    op.emit(j, p, dot, cf);
+    if (Op::kAxpy)
+      for (int64_t e = e0; e < e1; ++e) atomicAdd(&acc[rowidx[e]], cf * vals[e]);
+  }
+}
+
 template <class Op>
 static int run_csc(const int64_t* colptr, const int32_t* rowidx, const double* vals, int m,
                    int64_t n, const double* z, double* out, const double* sub, const Op& op,
@@ -1240,7 +1367,23 @@ static int run_csc(const int64_t* colptr, const int32_t* rowidx, const double* v
                    const void* ell = nullptr) {
   if (m < 1 || n < 0) return SKB_ERR_ARG;
   const size_t smem = (size_t)((Op::kDot ? m : 0) + (Op::kAxpy ? m : 0)) * 8;
-  if (smem > 220 * 1024) return SKB_ERR_UNSUPPORTED;  // m <= 14080 with both vectors
+  if (smem > 220 * 1024) {  // m > 14080 with both vectors (28160 with one)
+    double* acc = nullptr;
+    if (Op::kAxpy) {
+      acc = (double*)skb_ws_take(ws, (size_t)m * 8);
+      if (!acc) return SKB_ERR_WORKSPACE;
+      cudaMemsetAsync(acc, 0, (size_t)m * 8, st);
+    }
+    if (n > 0) {
+      const int grid = (int)std::max<int64_t>(
+          1, std::min<int64_t>((int64_t)skb_num_sms() * 8, (n + 255) / 256));
+      csc_global_kernel<Op><<<grid, 256, 0, st>>>(colptr, rowidx, vals, n, z, acc, op, gate);
+    }
+    if (Op::kAxpy)
+      reduce_partials_kernel<<<(m + 31) / 32, 256, 0, st>>>(acc, n > 0 ? 1 : 0, m, sub, out,
+                                                            gate);
+    return skb_launch_status(__func__);
+  }
   const int per_sm = smem <= 100 * 1024 ? 2 : 1;
   int grid = skb_num_sms() * per_sm;
   const int thr = (Op::kDot || !Op::kAxpy) ? kCscThreads : 512;

@@ -84,8 +84,10 @@ def test_lemire_draws_with_rejections(K):
 
 # ---------------------------------------------------------- column streams
 
+# m > ~13,900 (and > 16,384): the two-pass global-memory fallback of the dense passes
 SHAPES = [(1, 7), (20, 600), (63, 1000), (100, 10_000), (257, 3000), (1000, 5000),
-          (1001, 4001), (1025, 3000), (2000, 3000), (3001, 2500), (5000, 1200)]
+          (1001, 4001), (1025, 3000), (2000, 3000), (3001, 2500), (5000, 1200),
+          (16_000, 700), (20_001, 333)]
 
 
 def _problem(m, n, seed=0):

@@ -95,7 +95,9 @@ def test_csc_sketch_apply_bit_exact(K):
                                               (2500, 10_000, 5, 600, 4, True),
                                               (2500, 10_000, 0, 700, 4, False),
                                               (2500, 20_000, 5, 4, 2, False),
-                                              (2500, 20_000, 0, 3, 2, False)])
+                                              (2500, 20_000, 0, 3, 2, False),
+                                              (20_000, 2000, 5, 50, 4, False),
+                                              (30_000, 1000, 5, 40, 1, False)])
 def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix, kernel):
     """m > 2048 takes the warp-per-bucket L2 kernel: few buckets (many repeated
     rows per member chunk -> the ordered path) and columns longer than its
@@ -106,7 +108,9 @@ def test_csc_sketch_large_m_bit_exact(K, monkeypatch, m, n, k, w, s, radix, kern
     bucket, rows binned to owner warps; k = 0: ragged columns of 0..12 entries, the
     long ones split a batch), its bid-round variant (SKB_CSC_SKETCH_BIDS=1) or the L2
     kernel (SKB_CSC_SKETCH_L2=1). w = 3-4: 1e4+ members per bucket, several chunks of the
-    row-sorting kernel (later chunks continue each row from X)."""
+    row-sorting kernel (later chunks continue each row from X). m = 2e4 / 3e4: past the
+    bid-round kernel's (and at 3e4 the row-sorting kernel's) shared-memory ceiling, where
+    the dispatch falls back to the next kernel that fits."""
     from paper_2209_08722_b200 import sketching as S
     from paper_2209_08722_b200.lp_model import DeviceLP, LinearProgram
     if radix:
@@ -165,3 +169,30 @@ def test_sparse_trajectory_s4(K, monkeypatch, planned):
     dev = np.abs(np.array(rep.mu_trace) - np.array(gold["mu_trace"])) / np.array(gold["mu_trace"])
     assert np.all(dev <= np.maximum(1e-9, 4 * floor)), (dev, floor)
     assert abs(rep.objective - gold["objective"]) <= 1e-8 * abs(gold["objective"])
+
+
+@pytest.mark.parametrize("m", [20_000, 40_000])
+def test_csc_passes_past_shared_memory_ceiling(K, m):
+    """m past the shared-memory CSC kernels' ceiling (z and the partial m-vector:
+    m <= 14,080; one vector: m <= 28,160): the global-memory pass. Normal operator,
+    A x - sub and A'y against scipy."""
+    from paper_2209_08722_b200.kernels import SparseDeviceMatrix
+    g = np.random.Generator(np.random.Philox(m))
+    n = 3 * m
+    rows = np.stack([g.choice(m, size=5, replace=False) for _ in range(n)])
+    A = sp.csc_matrix((g.standard_normal(5 * n), rows.reshape(-1), np.arange(0, 5 * n + 1, 5)),
+                      shape=(m, n))
+    Ad = SparseDeviceMatrix.from_host(A)
+    d2 = 10.0 ** g.uniform(-2, 2, n)
+    z, x, y = g.standard_normal(m), g.standard_normal(n), g.standard_normal(m)
+    sub = g.standard_normal(m)
+    u = torch.empty(m, dtype=torch.float64, device="cuda")
+    K.normal_apply(Ad, _t(d2), _t(z), u, sub=_t(sub))
+    ref = A @ (d2 * (A.T @ z)) - sub
+    scale = (abs(A) @ (d2 * (abs(A.T) @ abs(z)))).max()
+    assert np.max(np.abs(_h(u) - ref)) <= 1e-13 * scale
+    K.gemv(Ad, _t(x), u)
+    assert np.max(np.abs(_h(u) - A @ x)) <= 1e-13 * (abs(A) @ abs(x)).max()
+    t = torch.empty(n, dtype=torch.float64, device="cuda")
+    K.gemv_t(Ad, _t(y), t)
+    assert np.max(np.abs(_h(t) - A.T @ y)) <= 1e-13 * (abs(A.T) @ abs(y)).max()
