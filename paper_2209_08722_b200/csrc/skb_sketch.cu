@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kConsumers + 32, KP <= 4 ? 2 : 1)
                              int w, int stages, unsigned int* __restrict__ counter,
                              double* __restrict__ X, int64_t ldx) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const size_t col_bytes = (size_t)lda * 8;
+  const size_t col_bytes = (size_t)((m + 1) & ~1) * 8;  // this row slice of a column
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + stages;
   StageMeta* meta = reinterpret_cast<StageMeta*>(empty + stages);
@@ -1141,22 +1141,11 @@ extern "C" int skb_csc_sketch_apply(const int64_t* colptr, const int32_t* rowidx
   return skb_launch_status(__func__);
 }
 
-extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda,
-                                const double* d, const int32_t* cols, const double* vals,
-                                int32_t s, int32_t w, double* X, int64_t ldx, void* workspace,
-                                size_t ws_bytes, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  if (m < 1 || m > 16384 || lda < m || (lda & 1) || ldx < m || (ldx & 1) || s < 1 || w < 1)
-    return SKB_ERR_ARG;
-  skb_ws ws = skb_ws_make(workspace, ws_bytes);
-  uint64_t* start;
-  int32_t* mem_e;
-  unsigned int* counter;
-  {
-    int rc0 = bucket_sort(cols, vals, n, s, w, &ws, st, &start, &mem_e, &counter);
-    if (rc0) return rc0;
-  }
-  const size_t col_bytes = (size_t)lda * 8;
+// One launch of the bucket-streaming kernel over rows [0, m) of A / X (a slice).
+static int sketch_slice(const double* A, int64_t lda, int64_t m, const double* d,
+                        const uint64_t* start, const int32_t* mem_e, const double* vals, int s,
+                        int w, unsigned int* counter, double* X, int64_t ldx, cudaStream_t st) {
+  const size_t col_bytes = (size_t)(m + (m & 1)) * 8;
   // tuning knobs (development): CTAs per SM and ring depth
   // Two CTAs per SM (two producers per SM): 1.73 -> 1.32 ms at c2 (round-1 sweep).
   // CTAs (bulk-copy producers) per SM: 4 for m <= 1024 (c2 s = 4: 4.91 -> 4.72 ms with 6
@@ -1196,6 +1185,35 @@ extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t l
     launch(sketch_accumulate_kernel<16>, 4);
   else
     launch(sketch_accumulate_kernel<32>, 5);
+  return rc;
+}
+
+extern "C" int skb_sketch_apply(const double* A, int64_t m, int64_t n, int64_t lda,
+                                const double* d, const int32_t* cols, const double* vals,
+                                int32_t s, int32_t w, double* X, int64_t ldx, void* workspace,
+                                size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < 1 || lda < m || (lda & 1) || ldx < m || (ldx & 1) || s < 1 || w < 1)
+    return SKB_ERR_ARG;
+  skb_ws ws = skb_ws_make(workspace, ws_bytes);
+  uint64_t* start;
+  int32_t* mem_e;
+  unsigned int* counter;
+  {
+    int rc0 = bucket_sort(cols, vals, n, s, w, &ws, st, &start, &mem_e, &counter);
+    if (rc0) return rc0;
+  }
+  // Rows are independent sums: past two staged columns per ring (m > ~12,800) the
+  // sketch runs over 8192-row slices of A and X (the same chains, bit-exact).
+  const int64_t m_full = m;
+  const bool sliced = (size_t)2 * (m + (m & 1)) * 8 + 256 > (size_t)200 * 1024;
+  const int64_t ms_max = sliced ? 8192 : m;
+  int rc = 0;
+  for (int64_t r0 = 0; r0 < m_full && !rc; r0 += ms_max) {
+    const int64_t ms = std::min<int64_t>(ms_max, m_full - r0);
+    if (r0 > 0) cudaMemsetAsync(counter, 0, 16, st);  // the bucket counter, per launch
+    rc = sketch_slice(A + r0, lda, ms, d, start, mem_e, vals, s, w, counter, X + r0, ldx, st);
+  }
   if (rc) return rc;
   return skb_launch_status(__func__);
 }

@@ -61,7 +61,8 @@ def test_sketch_apply_golden_bits(P):
 @pytest.mark.parametrize("m,n,w,s", [(100, 10_000, 400, 1), (100, 10_000, 400, 4),
                                      (37, 5000, 300, 2), (1000, 20_000, 4000, 1),
                                      (700, 8000, 2000, 3), (2000, 6000, 4000, 1),
-                                     (3000, 4000, 3500, 2), (1000, 30_000, 4000, 4)])
+                                     (3000, 4000, 3500, 2), (1000, 30_000, 4000, 4),
+                                     (13_001, 700, 300, 2)])  # 8192-row slices
 def test_sketch_apply_bit_exact_vs_c_oracle(P, monkeypatch, m, n, w, s):
     from paper_2209_08722_b200 import sketching as S
     if s == 4:  # the radix-sort bucket order (default from 2^20 entries) on the s = 4 cases
